@@ -1,0 +1,194 @@
+/* dsdv — C-ABI of the B200 adaptive speculative verifier (DSD, arXiv 2511.11733).
+ *
+ * This is the drop-in boundary between host code (the C++ `dsd::` API in
+ * include/dsd/, Python ctypes, or any FFI) and the sm_100a kernels in
+ * paper_2511_11733_b200/csrc/. No C++ or torch types cross it: plain pointers,
+ * sizes and POD structs only. All device pointers are caller-owned.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   dsdv_verify          <- dsd::verify_round        proj/src/verifier.cpp:215-257
+ *                           (whole window: is_key :136-159, soften :161-186,
+ *                            accept_prob :188-196, first-rejection break :223-250,
+ *                            residual_distribution :198-213, bonus draw :253-256)
+ *   dsdv_window_stats    <- the per-position front half of the same loop
+ *                           (token_cross_entropy :112-117, norm_match :119-134,
+ *                            is_key, soften's normaliser, accept_prob) for callers
+ *                            that own their UniformStream (proj/include/dsd/rng.hpp:25-29)
+ *   dsdv_sample_extra    <- residual_distribution + sample (verifier.cpp:245-246)
+ *                           and the bonus draw (verifier.cpp:253-256) with
+ *                           sample_with_uniform semantics (distribution.cpp:103-114)
+ *   dsdv_draft_sample    <- draft_window's per-position inverse-CDF draw
+ *                           (verifier.cpp:93-110 -> distribution.cpp:99-114)
+ *   dsdv_status codes    <- dsd::Error tree (proj/include/dsd/error.hpp:24-71)
+ *   dsdv_uniform         <- UniformStream::next_uniform (rng.hpp:25-40), counter form
+ *
+ * Data layout in HBM (row-major, vocabulary contiguous):
+ *   draft_logits [batch][gamma    ][row_stride]
+ *   target_logits[batch][gamma + 1][row_stride]   (row gamma feeds the bonus draw)
+ *   draft_tokens [batch][gamma] int32
+ * Only the first vocab_local entries of a row are read as logits; the kernels
+ * stream rows with 1-D bulk (TMA) copies, so row_stride * sizeof(dtype) must be a
+ * multiple of 16 bytes and the base pointers 16-byte aligned.
+ *
+ * Inputs are logits (natural-log scale, -inf allowed for unsupported tokens).
+ * The reference works on probability vectors; P = softmax(logits) is the
+ * front end it lacks (its Distribution::from_weights, distribution.cpp:54-63).
+ */
+#ifndef DSDV_DSDV_H_
+#define DSDV_DSDV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSDV_ABI_VERSION 1
+
+typedef struct dsdv_ctx dsdv_ctx; /* one per host thread / stream; no globals */
+
+typedef enum {
+  DSDV_OK = 0,
+  DSDV_E_INVARIANT = 1,          /* dsd::InvariantError          error.hpp:30 */
+  DSDV_E_DEGENERATE_MIXTURE = 2, /* dsd::DegenerateMixtureError  error.hpp:41 */
+  DSDV_E_DRAFTING_CONTRACT = 3,  /* dsd::DraftingContractError   error.hpp:47 */
+  DSDV_E_EMPTY_RESIDUAL = 4,     /* dsd::EmptyResidualError      error.hpp:53 */
+  DSDV_E_CUDA = 5,               /* device / driver failure (no reference analogue) */
+  DSDV_E_NCCL = 6,               /* collective failure (sharded verifier) */
+  DSDV_E_UNSUPPORTED = 7         /* shape outside what the kernels accept */
+} dsdv_status;
+
+typedef enum { DSDV_DTYPE_F32 = 0, DSDV_DTYPE_BF16 = 1, DSDV_DTYPE_F64 = 2 } dsdv_dtype;
+
+/* Order of dsd::ExtraSource (verifier.hpp:65-68). */
+typedef enum { DSDV_EXTRA_BONUS = 0, DSDV_EXTRA_RESIDUAL = 1 } dsdv_extra_source;
+
+/* Kind of effective distribution used at a position (verifier.cpp:231-233,
+ * soften's short-circuits :170-172). */
+typedef enum {
+  DSDV_EFF_TARGET = 0,   /* key token, tau == 0, or target row == draft row */
+  DSDV_EFF_DRAFT = 1,    /* non-key, tau == 1 */
+  DSDV_EFF_SOFTENED = 2  /* non-key, 0 < tau < 1: softmax((1-tau) l_t + tau l_d) */
+} dsdv_effective_kind;
+
+typedef struct {
+  int32_t batch;        /* B >= 1 */
+  int32_t gamma;        /* draft window length >= 1           (VerifyParams::gamma) */
+  int32_t vocab;        /* V >= 2, global vocabulary size */
+  int32_t row_stride;   /* elements between consecutive rows */
+  int32_t dtype;        /* dsdv_dtype of the logits; F64 computes in fp64 */
+  int32_t top_m;        /* >= 1, clamped to V at use           (KeyCriteria::top_m) */
+  double tau;           /* [0, 1]                              (VerifyParams::tau) */
+  double ratio_limit;   /* > 0, may be +inf                    (KeyCriteria) */
+  double gap_limit;     /* [0, 1] */
+  double overlap_floor; /* [0, 1] */
+  uint64_t seed;        /* Philox key (include/dsdv/philox.h) */
+  uint64_t window;      /* Philox counter words 2-3: verification window index */
+  uint32_t sequence_offset; /* Philox counter word 1 = sequence_offset + b */
+  int32_t vocab_offset; /* sharded verifier: first global id of this slice (0 when unsharded) */
+  int32_t vocab_local;  /* sharded verifier: ids in this slice (== vocab when unsharded) */
+  double eps_u;         /* near-threshold band for |u - a| (counted, reported) */
+  double eps_lambda;    /* relative band for |clause - lambda| */
+} dsdv_params;
+
+/* Per-position record kept between dsdv_window_stats and dsdv_sample_extra
+ * (natural-log normalisers of P_t, P_d and the softened mix, and the kind of
+ * effective distribution). Layout: double[batch][gamma + 1][DSDV_RECORD_WORDS]. */
+#define DSDV_RECORD_WORDS 8
+
+typedef struct {
+  /* per sequence, [batch] (required by dsdv_verify, ignored by window_stats) */
+  int32_t *accepted_count;   /* k (VerificationResult::accepted_count) */
+  int32_t *extra_token;      /* VerificationResult::extra_token */
+  uint8_t *extra_source;     /* dsdv_extra_source */
+  int32_t *key_count;        /* key tokens among the evaluated positions */
+  int32_t *status;           /* dsdv_status of the sequence (0 = ok) */
+  int32_t *near_threshold;   /* evaluated draws/clauses inside the eps bands */
+  /* per position, [batch][gamma], optional (NULL skips). Positions past the
+   * first rejection are computed too but are not part of the round. */
+  uint8_t *key_mask;         /* TokenDecision::is_key */
+  uint8_t *accepted;         /* TokenDecision::accepted (u < accept_prob) */
+  double *accept_prob;       /* TokenDecision::accept_prob */
+  double *h_target;          /* -ln P_t(y)   (token_cross_entropy) */
+  double *h_draft;           /* -ln P_d(y) */
+  double *p_target_y;        /* P_t(y) */
+  double *p_draft_y;         /* P_d(y) */
+  double *norm_match;        /* top-m overlap, multiple of 1/m */
+  double *p_effective_y;     /* P_eff(y): P_t for key tokens, softened otherwise */
+  double *uniform;           /* the accept draw u at this position */
+  /* [batch][gamma + 1][DSDV_RECORD_WORDS], optional for dsdv_verify,
+   * required by dsdv_window_stats -> dsdv_sample_extra */
+  double *records;
+} dsdv_outputs;
+
+/* ---- lifetime ---------------------------------------------------------- */
+dsdv_status dsdv_create(int device, dsdv_ctx **out);
+dsdv_status dsdv_destroy(dsdv_ctx *ctx);
+/* Message of the last failing call on ctx; with ctx == NULL, of the last
+ * context-free call (dsdv_validate(NULL, ...)) on this host thread. */
+const char *dsdv_last_error(const dsdv_ctx *ctx);
+int dsdv_abi_version(void);
+
+/* Host-side validation only (VerifyParams::validate, verifier.cpp:55-91, plus
+ * layout checks). Every entry point below runs it before launching. ctx may
+ * be NULL (no device needed). */
+dsdv_status dsdv_validate(dsdv_ctx *ctx, const dsdv_params *params);
+
+/* ---- the hot path ------------------------------------------------------ */
+/* One verification window for all B sequences in ONE fused persistent kernel:
+ * softmax statistics, surprisals, gap, NormMatch, key flags, softened
+ * normaliser, accept test with Philox draws, first-rejection scan and the
+ * residual / bonus draw. Asynchronous on `stream` (a cudaStream_t). */
+dsdv_status dsdv_verify(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,
+                        const void *target_logits, const int32_t *draft_tokens,
+                        const dsdv_outputs *out, void *stream);
+
+/* Statistics and accept probabilities for every position, no draws. Fills the
+ * per-position outputs, records, and status[B] (first error position, as the
+ * reference would raise it walking left to right with all positions evaluated). */
+dsdv_status dsdv_window_stats(dsdv_ctx *ctx, const dsdv_params *params,
+                              const void *draft_logits, const void *target_logits,
+                              const int32_t *draft_tokens, const dsdv_outputs *out,
+                              void *stream);
+
+/* Extra token per sequence from the records of dsdv_window_stats:
+ * position[b] < gamma -> residual of that position's effective distribution
+ * against P_d; position[b] == gamma -> bonus draw from target row gamma.
+ * uniform[b] is the caller's draw. status[b] gets DSDV_E_EMPTY_RESIDUAL when
+ * the residual has no mass. */
+dsdv_status dsdv_sample_extra(dsdv_ctx *ctx, const dsdv_params *params,
+                              const void *draft_logits, const void *target_logits,
+                              const double *records, const int32_t *position,
+                              const double *uniform, int32_t *token_out, int32_t *status,
+                              void *stream);
+
+/* Draft-side step: tokens[b][j] = inverse-CDF draw from softmax(draft row j)
+ * with the Philox draft slot j (philox.h). */
+dsdv_status dsdv_draft_sample(dsdv_ctx *ctx, const dsdv_params *params,
+                              const void *draft_logits, int32_t *draft_tokens, void *stream);
+
+/* Waits for `stream`, then reports the first failing sequence's status with a
+ * reference-style message in dsdv_last_error (status may be NULL to only sync). */
+dsdv_status dsdv_sync(dsdv_ctx *ctx, const dsdv_params *params, const int32_t *status,
+                      void *stream);
+
+/* ---- helpers ----------------------------------------------------------- */
+/* The accept / extra / draft uniform the kernels use (philox.h), on the host. */
+double dsdv_uniform(uint64_t seed, uint64_t window, uint32_t sequence, uint32_t slot);
+
+/* Benchmark / test inputs: seeded synthetic logits of the four row families
+ * of SURVEY.md §8(d) (b mod 4: Zipf sigma 1.2/2.5/3.5 and Gaussian sigma 6;
+ * draft = target + delta * N(0,1)). Writes draft [B][gamma] and target
+ * [B][gamma+1] rows (dtype F32 or BF16). Not part of the verifier. */
+dsdv_status dsdv_synth_logits(dsdv_ctx *ctx, const dsdv_params *params, uint64_t logits_seed,
+                              void *draft_logits, void *target_logits, void *stream);
+
+/* Number of kernel launches issued by this context so far (bench evidence). */
+uint64_t dsdv_launch_count(const dsdv_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DSDV_DSDV_H_ */

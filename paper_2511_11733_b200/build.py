@@ -1,0 +1,93 @@
+"""In-tree build of the native libraries (nvcc / g++, no torch JIT cache).
+
+    libdsdv.so      sm_100a kernels + the C-ABI of include/dsdv/dsdv.h
+    libdsd_b200.so  the C++ drop-in `dsd::` verifier API (include/dsd/) over the C-ABI
+
+Outputs land next to this file so they travel with a gpurun snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+HOSTSRC = PKG / "host"
+INCLUDE = ROOT / "include"
+BUILD = ROOT / "build"
+
+LIB_DSDV = PKG / "libdsdv.so"
+LIB_DSD = PKG / "libdsd_b200.so"
+
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+              f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
+
+CU_SOURCES = ["verify.cu", "rows.cu", "abi.cu"]
+HOST_SOURCES = ["dsd_api.cpp"]
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("build step failed: " + " ".join(cmd))
+
+
+def _stale(out: Path, deps: list[Path]) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def _headers() -> list[Path]:
+    return sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.rglob("*.h")) + sorted(INCLUDE.rglob("*.hpp"))
+
+
+def build_dsdv(force: bool = False) -> Path:
+    hdrs = _headers()
+    if not force and not _stale(LIB_DSDV, [*(CSRC / s for s in CU_SOURCES), *hdrs]):
+        return LIB_DSDV  # up to date (also on GPU boxes, where build/ is not shipped)
+    BUILD.mkdir(exist_ok=True)
+    objs = []
+    jobs = []
+    for src in CU_SOURCES:
+        s = CSRC / src
+        o = BUILD / (s.stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [s, *hdrs]):
+            jobs.append([NVCC, *NVCC_FLAGS, "-c", str(s), "-o", str(o)])
+    with ThreadPoolExecutor(max_workers=min(4, max(1, len(jobs)))) as ex:
+        list(ex.map(_run, jobs))
+    if force or jobs or _stale(LIB_DSDV, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIB_DSDV), *map(str, objs)])
+    return LIB_DSDV
+
+
+def build_dsd_api(force: bool = False) -> Path | None:
+    srcs = [HOSTSRC / s for s in HOST_SOURCES if (HOSTSRC / s).exists()]
+    if not srcs:
+        return None
+    deps = [*srcs, *_headers(), LIB_DSDV]
+    if force or _stale(LIB_DSD, deps):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
+              f"-I{INCLUDE}", *map(str, srcs), "-o", str(LIB_DSD),
+              f"-L{PKG}", "-ldsdv", "-Wl,-rpath,$ORIGIN"])
+    return LIB_DSD
+
+
+def build_all(force: bool = False) -> None:
+    build_dsdv(force)
+    build_dsd_api(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)
+    print(LIB_DSDV)

@@ -1,0 +1,448 @@
+// C-ABI entry points (include/dsdv/dsdv.h): validation with the reference's
+// messages, scratch management, dtype dispatch and error mapping.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dsdv {
+int fused_max_vocab(int esize);
+template <class In>
+cudaError_t launch_fused(const DevParams &, const void *, const void *, const int32_t *,
+                         const DevOut &, const DevScratch &, cudaStream_t, int *);
+template <class In>
+cudaError_t launch_sample_extra(const DevParams &, const void *, const void *, const double *,
+                                const int32_t *, const double *, int32_t *, int32_t *,
+                                cudaStream_t);
+template <class In>
+cudaError_t launch_draft_sample(const DevParams &, const void *, int32_t *, cudaStream_t);
+cudaError_t launch_synth(int dtype, int B, int gamma, int V, int stride, uint64_t seed,
+                         void *draft, void *target, cudaStream_t stream);
+}  // namespace dsdv
+
+struct dsdv_ctx {
+  int device = 0;
+  std::string last_error;
+  unsigned int *counters = nullptr;  // [0] ticket, [1] exit count
+  unsigned int *flags = nullptr;  // [positions]
+  int2 *slots = nullptr;          // [positions]
+  unsigned int *done = nullptr;   // [sequences]
+  size_t flags_cap = 0;
+  size_t done_cap = 0;
+  uint32_t epoch = 0;
+  uint64_t launches = 0;
+  int last_grid = 0;
+};
+
+namespace {
+
+using dsdv::DevOut;
+using dsdv::DevParams;
+using dsdv::DevScratch;
+
+// Messages of calls made without a context (host-only validation).
+thread_local std::string g_host_error;
+
+dsdv_status fail(dsdv_ctx *ctx, dsdv_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  (ctx ? ctx->last_error : g_host_error) = buf;
+  return st;
+}
+
+// std::to_string(double) formatting, as the reference messages use it.
+std::string dstr(double x) {
+  char b[64];
+  snprintf(b, sizeof(b), "%f", x);
+  return b;
+}
+
+dsdv_status cuda_fail(dsdv_ctx *ctx, cudaError_t e, const char *what) {
+  return fail(ctx, DSDV_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int esize(int dtype) {
+  return dtype == DSDV_DTYPE_BF16 ? 2 : (dtype == DSDV_DTYPE_F32 ? 4 : 8);
+}
+
+dsdv_status ensure_scratch(dsdv_ctx *ctx, size_t n_positions, size_t n_sequences) {
+  cudaError_t e;
+  if (!ctx->counters) {
+    e = cudaMalloc(&ctx->counters, 2 * sizeof(unsigned int));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(counters)");
+    e = cudaMemset(ctx->counters, 0, 2 * sizeof(unsigned int));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemset(counters)");
+  }
+  if (n_positions > ctx->flags_cap) {
+    if (ctx->flags) cudaFree(ctx->flags);
+    e = cudaMalloc(&ctx->flags, n_positions * sizeof(unsigned int));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(flags)");
+    e = cudaMemset(ctx->flags, 0, n_positions * sizeof(unsigned int));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemset(flags)");
+    if (ctx->slots) cudaFree(ctx->slots);
+    e = cudaMalloc(&ctx->slots, n_positions * sizeof(int2));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(slots)");
+    ctx->flags_cap = n_positions;
+    ctx->epoch = 0;
+  }
+  if (n_sequences > ctx->done_cap) {
+    if (ctx->done) cudaFree(ctx->done);
+    e = cudaMalloc(&ctx->done, n_sequences * sizeof(unsigned int));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(done)");
+    e = cudaMemset(ctx->done, 0, n_sequences * sizeof(unsigned int));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemset(done)");
+    ctx->done_cap = n_sequences;
+  }
+  return DSDV_OK;
+}
+
+dsdv_status build_params(dsdv_ctx *ctx, const dsdv_params *pp, DevParams &d) {
+  dsdv_status st = dsdv_validate(ctx, pp);
+  if (st != DSDV_OK) return st;
+  const dsdv_params &p = *pp;
+  std::memset(&d, 0, sizeof(d));
+  d.B = p.batch;
+  d.gamma = p.gamma;
+  d.V = p.vocab;
+  d.stride = p.row_stride;
+  d.top_m = p.top_m < p.vocab ? p.top_m : p.vocab;  // clamp, verifier.cpp:155
+  d.vocab_offset = p.vocab_offset;
+  d.vocab_local = p.vocab_local;
+  const int chunk_elems = dsdv::kChunkBytes / esize(p.dtype);
+  d.n_chunks = (p.vocab_local + chunk_elems - 1) / chunk_elems;
+  d.n_items = p.batch * (p.gamma + 1);
+  d.stats_only = 0;
+  d.need_z = (p.tau > 0.0 && p.tau < 1.0) ? 1 : 0;
+  d.tau_f = (float)p.tau;
+  d.omt_f = (float)(1.0 - p.tau);
+  d.tau = p.tau;
+  d.ratio_limit = p.ratio_limit;
+  d.gap_limit = p.gap_limit;
+  d.overlap_floor = p.overlap_floor;
+  d.eps_u = p.eps_u;
+  d.eps_lambda = p.eps_lambda;
+  d.seed = p.seed;
+  d.window = p.window;
+  d.seq_offset = p.sequence_offset;
+  return DSDV_OK;
+}
+
+DevOut to_dev(const dsdv_outputs *o) {
+  DevOut d;
+  std::memset(&d, 0, sizeof(d));
+  if (!o) return d;
+  d.accepted_count = o->accepted_count;
+  d.extra_token = o->extra_token;
+  d.key_count = o->key_count;
+  d.status = o->status;
+  d.near_threshold = o->near_threshold;
+  d.extra_source = o->extra_source;
+  d.key_mask = o->key_mask;
+  d.accepted = o->accepted;
+  d.accept_prob = o->accept_prob;
+  d.h_target = o->h_target;
+  d.h_draft = o->h_draft;
+  d.p_target_y = o->p_target_y;
+  d.p_draft_y = o->p_draft_y;
+  d.norm_match = o->norm_match;
+  d.p_effective_y = o->p_effective_y;
+  d.uniform = o->uniform;
+  d.records = o->records;
+  return d;
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draft,
+                      const void *target, const int32_t *tokens, const dsdv_outputs *out,
+                      void *stream, bool stats_only) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  DevParams d;
+  dsdv_status st = build_params(ctx, params, d);
+  if (st != DSDV_OK) return st;
+  d.stats_only = stats_only ? 1 : 0;
+  if (!draft || !target || !tokens || !out)
+    return fail(ctx, DSDV_E_INVARIANT, "logits, draft tokens and outputs must be non-null");
+  if (!aligned16(draft) || !aligned16(target))
+    return fail(ctx, DSDV_E_UNSUPPORTED, "logit base pointers must be 16-byte aligned");
+  if (!stats_only && (!out->accepted_count || !out->extra_token || !out->extra_source ||
+                      !out->key_count || !out->status || !out->near_threshold))
+    return fail(ctx, DSDV_E_INVARIANT,
+                "dsdv_verify: the per-sequence outputs (accepted_count, extra_token, "
+                "extra_source, key_count, status, near_threshold) are required");
+  if (stats_only && !out->records)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_window_stats: records output is required");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  st = ensure_scratch(ctx, (size_t)d.n_items, (size_t)d.B);
+  if (st != DSDV_OK) return st;
+  ctx->epoch = (ctx->epoch + 1) & 0x0fffffffu;
+  if (ctx->epoch == 0) {
+    cudaMemsetAsync(ctx->flags, 0, ctx->flags_cap * sizeof(unsigned int), (cudaStream_t)stream);
+    ctx->epoch = 1;
+  }
+  d.epoch = ctx->epoch;
+  DevScratch s;
+  s.ticket = ctx->counters;
+  s.exit_count = ctx->counters + 1;
+  s.flags = ctx->flags;
+  s.slots = ctx->slots;
+  s.done = ctx->done;
+  const DevOut o = to_dev(out);
+  switch (params->dtype) {
+    case DSDV_DTYPE_BF16:
+      e = dsdv::launch_fused<__nv_bfloat16>(d, draft, target, tokens, o, s, (cudaStream_t)stream,
+                                            &ctx->last_grid);
+      break;
+    case DSDV_DTYPE_F32:
+      e = dsdv::launch_fused<float>(d, draft, target, tokens, o, s, (cudaStream_t)stream,
+                                    &ctx->last_grid);
+      break;
+    default:
+      e = dsdv::launch_fused<double>(d, draft, target, tokens, o, s, (cudaStream_t)stream,
+                                     &ctx->last_grid);
+      break;
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "fused verifier launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dsdv_abi_version(void) { return DSDV_ABI_VERSION; }
+
+dsdv_status dsdv_create(int device, dsdv_ctx **out) {
+  if (!out) return DSDV_E_INVARIANT;
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0 || device < 0 || device >= n) return DSDV_E_CUDA;
+  dsdv_ctx *ctx = new dsdv_ctx();
+  ctx->device = device;
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return DSDV_E_CUDA;
+  }
+  if (ensure_scratch(ctx, 1, 1) != DSDV_OK) {
+    delete ctx;
+    return DSDV_E_CUDA;
+  }
+  *out = ctx;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_destroy(dsdv_ctx *ctx) {
+  if (!ctx) return DSDV_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->counters) cudaFree(ctx->counters);
+  if (ctx->flags) cudaFree(ctx->flags);
+  if (ctx->slots) cudaFree(ctx->slots);
+  if (ctx->done) cudaFree(ctx->done);
+  delete ctx;
+  return DSDV_OK;
+}
+
+const char *dsdv_last_error(const dsdv_ctx *ctx) {
+  return ctx ? ctx->last_error.c_str() : g_host_error.c_str();
+}
+
+uint64_t dsdv_launch_count(const dsdv_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+double dsdv_uniform(uint64_t seed, uint64_t window, uint32_t sequence, uint32_t slot) {
+  return dsdv_philox_uniform(seed, window, sequence, slot);
+}
+
+// VerifyParams::validate + KeyCriteria::validate (verifier.cpp:55-91), same
+// messages, then the layout rules of this ABI.
+dsdv_status dsdv_validate(dsdv_ctx *ctx, const dsdv_params *pp) {
+  if (!pp) return fail(ctx, DSDV_E_INVARIANT, "null parameters");
+  const dsdv_params &p = *pp;
+  if (p.gamma < 1)
+    return fail(ctx, DSDV_E_INVARIANT, "gamma must be >= 1, got %d", p.gamma);
+  if (!std::isfinite(p.tau) || p.tau < 0.0 || p.tau > 1.0)
+    return fail(ctx, DSDV_E_INVARIANT, "tau must lie in [0, 1], got %s", dstr(p.tau).c_str());
+  if (std::isnan(p.ratio_limit) || p.ratio_limit <= 0.0)
+    return fail(ctx, DSDV_E_INVARIANT, "criteria.ratio_limit must be > 0, got %s",
+                dstr(p.ratio_limit).c_str());
+  if (!std::isfinite(p.gap_limit) || p.gap_limit < 0.0 || p.gap_limit > 1.0)
+    return fail(ctx, DSDV_E_INVARIANT, "criteria.gap_limit must lie in [0, 1], got %s",
+                dstr(p.gap_limit).c_str());
+  if (!std::isfinite(p.overlap_floor) || p.overlap_floor < 0.0 || p.overlap_floor > 1.0)
+    return fail(ctx, DSDV_E_INVARIANT, "criteria.overlap_floor must lie in [0, 1], got %s",
+                dstr(p.overlap_floor).c_str());
+  if (p.top_m < 1)
+    return fail(ctx, DSDV_E_INVARIANT, "criteria.top_m must be >= 1, got %d", p.top_m);
+  if (p.batch < 1) return fail(ctx, DSDV_E_INVARIANT, "batch must be >= 1, got %d", p.batch);
+  if (p.vocab < 2)
+    return fail(ctx, DSDV_E_INVARIANT,
+                "distribution needs a vocabulary of at least 2 tokens, got %d", p.vocab);
+  if (p.dtype != DSDV_DTYPE_F32 && p.dtype != DSDV_DTYPE_BF16 && p.dtype != DSDV_DTYPE_F64)
+    return fail(ctx, DSDV_E_UNSUPPORTED, "unknown logits dtype %d", p.dtype);
+  if (p.vocab_local < 1 || p.vocab_offset < 0 || p.vocab_offset + p.vocab_local > p.vocab)
+    return fail(ctx, DSDV_E_INVARIANT, "vocab slice [%d, %d) outside vocabulary of size %d",
+                p.vocab_offset, p.vocab_offset + p.vocab_local, p.vocab);
+  const int es = esize(p.dtype), vec = 16 / es;
+  const int need = (p.vocab_local + vec - 1) / vec * vec;
+  if (p.row_stride < need || ((size_t)p.row_stride * es) % 16 != 0)
+    return fail(ctx, DSDV_E_UNSUPPORTED,
+                "row_stride %d must be >= %d and a multiple of %d elements (16-byte rows)",
+                p.row_stride, need, vec);
+  if (p.vocab_local > dsdv::fused_max_vocab(es))
+    return fail(ctx, DSDV_E_UNSUPPORTED, "vocab slice %d exceeds the fused kernel limit %d for this dtype",
+                p.vocab_local, dsdv::fused_max_vocab(es));
+  const int m = p.top_m < p.vocab ? p.top_m : p.vocab;
+  if (m > dsdv::kMaxTopM)
+    return fail(ctx, DSDV_E_UNSUPPORTED, "top_m %d exceeds the kernel limit %d", m,
+                dsdv::kMaxTopM);
+  if (!(p.eps_u >= 0.0) || !(p.eps_lambda >= 0.0))
+    return fail(ctx, DSDV_E_INVARIANT, "eps bands must be >= 0");
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_verify(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,
+                        const void *target_logits, const int32_t *draft_tokens,
+                        const dsdv_outputs *out, void *stream) {
+  return run_fused(ctx, params, draft_logits, target_logits, draft_tokens, out, stream, false);
+}
+
+dsdv_status dsdv_window_stats(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,
+                              const void *target_logits, const int32_t *draft_tokens,
+                              const dsdv_outputs *out, void *stream) {
+  return run_fused(ctx, params, draft_logits, target_logits, draft_tokens, out, stream, true);
+}
+
+dsdv_status dsdv_sample_extra(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,
+                              const void *target_logits, const double *records,
+                              const int32_t *position, const double *uniform, int32_t *token_out,
+                              int32_t *status, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  DevParams d;
+  dsdv_status st = build_params(ctx, params, d);
+  if (st != DSDV_OK) return st;
+  if (!draft_logits || !target_logits || !records || !position || !uniform || !token_out || !status)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_sample_extra: null argument");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  switch (params->dtype) {
+    case DSDV_DTYPE_BF16:
+      e = dsdv::launch_sample_extra<__nv_bfloat16>(d, draft_logits, target_logits, records,
+                                                   position, uniform, token_out, status,
+                                                   (cudaStream_t)stream);
+      break;
+    case DSDV_DTYPE_F32:
+      e = dsdv::launch_sample_extra<float>(d, draft_logits, target_logits, records, position,
+                                           uniform, token_out, status, (cudaStream_t)stream);
+      break;
+    default:
+      e = dsdv::launch_sample_extra<double>(d, draft_logits, target_logits, records, position,
+                                            uniform, token_out, status, (cudaStream_t)stream);
+      break;
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "sample_extra launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_draft_sample(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,
+                              int32_t *draft_tokens, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  DevParams d;
+  dsdv_status st = build_params(ctx, params, d);
+  if (st != DSDV_OK) return st;
+  if (params->vocab_local != params->vocab || params->vocab_offset != 0)
+    return fail(ctx, DSDV_E_UNSUPPORTED, "dsdv_draft_sample needs the whole vocabulary");
+  if (!draft_logits || !draft_tokens)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_draft_sample: null argument");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  switch (params->dtype) {
+    case DSDV_DTYPE_BF16:
+      e = dsdv::launch_draft_sample<__nv_bfloat16>(d, draft_logits, draft_tokens,
+                                                   (cudaStream_t)stream);
+      break;
+    case DSDV_DTYPE_F32:
+      e = dsdv::launch_draft_sample<float>(d, draft_logits, draft_tokens, (cudaStream_t)stream);
+      break;
+    default:
+      e = dsdv::launch_draft_sample<double>(d, draft_logits, draft_tokens, (cudaStream_t)stream);
+      break;
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "draft_sample launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_synth_logits(dsdv_ctx *ctx, const dsdv_params *params, uint64_t logits_seed,
+                              void *draft_logits, void *target_logits, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  dsdv_status st = dsdv_validate(ctx, params);
+  if (st != DSDV_OK) return st;
+  if (params->dtype == DSDV_DTYPE_F64)
+    return fail(ctx, DSDV_E_UNSUPPORTED, "synthetic logits are f32 or bf16");
+  if (params->vocab_local != params->vocab)
+    return fail(ctx, DSDV_E_UNSUPPORTED, "synthetic logits cover the whole vocabulary");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  e = dsdv::launch_synth(params->dtype, params->batch, params->gamma, params->vocab,
+                         params->row_stride, logits_seed, draft_logits, target_logits,
+                         (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "synth launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_sync(dsdv_ctx *ctx, const dsdv_params *params, const int32_t *status,
+                      void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamSynchronize");
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel");
+  if (!status || !params) return DSDV_OK;
+  std::vector<int32_t> h((size_t)params->batch);
+  e = cudaMemcpy(h.data(), status, h.size() * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpy(status)");
+  for (size_t b = 0; b < h.size(); ++b) {
+    switch (h[b]) {
+      case DSDV_OK:
+        continue;
+      case DSDV_E_INVARIANT:
+        return fail(ctx, DSDV_E_INVARIANT,
+                    "sequence %zu: a logit row has no finite mass or a draft token lies outside "
+                    "the vocabulary of size %d",
+                    b, params->vocab);
+      case DSDV_E_DEGENERATE_MIXTURE:
+        return fail(ctx, DSDV_E_DEGENERATE_MIXTURE,
+                    "softened distribution has zero mass: target and draft supports are "
+                    "disjoint (sequence %zu)",
+                    b);
+      case DSDV_E_DRAFTING_CONTRACT:
+        return fail(ctx, DSDV_E_DRAFTING_CONTRACT,
+                    "drafted token has zero draft probability; it cannot have been drafted "
+                    "(sequence %zu)",
+                    b);
+      case DSDV_E_EMPTY_RESIDUAL:
+        return fail(ctx, DSDV_E_EMPTY_RESIDUAL,
+                    "residual is empty: effective and draft distributions match (sequence %zu)",
+                    b);
+      default:
+        return fail(ctx, (dsdv_status)h[b], "sequence %zu failed with status %d", b, h[b]);
+    }
+  }
+  return DSDV_OK;
+}
+
+}  // extern "C"

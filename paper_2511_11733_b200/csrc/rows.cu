@@ -1,0 +1,267 @@
+// Row-level kernels around the fused verifier:
+//   * sample_extra_kernel  — the extra draw from records of dsdv_window_stats,
+//     for callers that own their UniformStream (residual_distribution + sample,
+//     verifier.cpp:245-246; bonus draw :253-256);
+//   * draft_sample_kernel  — the draft-side step, inverse-CDF draws from
+//     softmax(draft row) (draft_window, verifier.cpp:93-110);
+//   * synth_logits_kernel  — seeded benchmark/test inputs.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "sample.cuh"
+
+namespace dsdv {
+
+struct RowsSmem {
+  SampleShared samp;
+  double red_m[kConsumerWarps], red_s[kConsumerWarps];
+};
+
+template <class In>
+__global__ void __launch_bounds__(kConsumerThreads)
+    sample_extra_kernel(const __grid_constant__ DevParams p, const In *__restrict__ draft,
+                        const In *__restrict__ target, const double *__restrict__ records,
+                        const int32_t *__restrict__ position, const double *__restrict__ uniform,
+                        int32_t *__restrict__ token_out, int32_t *__restrict__ status) {
+  using Acc = typename InTraits<In>::Acc;
+  __shared__ RowsSmem sm;
+  __shared__ Weigher<Acc> wf;
+  __shared__ int skip;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int G1 = p.gamma + 1;
+  const int j = position[b];
+  if (tid == 0) {
+    skip = 0;
+    if (j < 0 || j > p.gamma) {
+      token_out[b] = -1;
+      status[b] = DSDV_E_INVARIANT;
+      skip = 1;
+    } else {
+      const double *r = records + ((size_t)b * G1 + j) * kRecordWords;
+      const int flags = (int)r[kRecFlags];
+      const int kind = flags & 0xff, err = (flags >> 8) & 0xff;
+      PosEval ev;
+      ev.mt = r[kRecMt];
+      ev.lst = r[kRecLst];
+      ev.md = r[kRecMd];
+      ev.lsd = r[kRecLsd];
+      ev.lsz = r[kRecLsz];
+      if (err) {
+        token_out[b] = -1;
+        status[b] = err;
+        skip = 1;
+      } else if (j == p.gamma) {
+        set_weigher(wf, kWeightPlain, ev, (double)p.omt_f, (double)p.tau_f);
+      } else if (kind == DSDV_EFF_DRAFT) {
+        token_out[b] = -1;
+        status[b] = DSDV_E_EMPTY_RESIDUAL;
+        skip = 1;
+      } else {
+        set_weigher(wf, kind == DSDV_EFF_SOFTENED ? kWeightResSoft : kWeightResTarget, ev,
+                    (double)p.omt_f, (double)p.tau_f);
+      }
+    }
+  }
+  __syncthreads();
+  if (skip) return;
+  const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
+  const In *rd = draft + ((size_t)b * p.gamma + (j < p.gamma ? j : 0)) * (size_t)p.stride;
+  int near = 0;
+  const int idx = cdf_sample<In, Acc>(rt, rd, wf, p.vocab_local, uniform[b], p.eps_u, &sm.samp,
+                                      tid, &near);
+  if (tid == 0) {
+    if (idx < 0) {
+      token_out[b] = -1;
+      status[b] = DSDV_E_EMPTY_RESIDUAL;
+    } else {
+      token_out[b] = p.vocab_offset + idx;
+      status[b] = DSDV_OK;
+    }
+  }
+}
+
+template <class In>
+__global__ void __launch_bounds__(kConsumerThreads)
+    draft_sample_kernel(const __grid_constant__ DevParams p, const In *__restrict__ draft,
+                        int32_t *__restrict__ tokens) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int VEC = InTraits<In>::kVec;
+  __shared__ RowsSmem sm;
+  __shared__ Weigher<Acc> wf;
+  const int row = blockIdx.x;  // b * gamma + j
+  const int b = row / p.gamma, j = row - b * p.gamma;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const In *rd = draft + (size_t)row * p.stride;
+  const Acc ni = neg_inf<Acc>();
+  Acc m = ni, s = Acc(0);
+  const int nvec = (p.vocab_local + VEC - 1) / VEC;
+  for (int q = tid; q < nvec; q += kConsumerThreads) {
+    Acc v[VEC];
+    unpack(ldg128(rd + (size_t)q * VEC), v, (In *)nullptr);
+    Acc cm = ni;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      if (q * VEC + e >= p.vocab_local) v[e] = ni;
+      cm = v[e] > cm ? v[e] : cm;
+    }
+    Acc cs = Acc(0);
+    if (cm != ni) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) cs += fast_exp2((v[e] - cm) * log2e<Acc>());
+    }
+    merge_ms(m, s, cm, cs);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const Acc m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const Acc s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    merge_ms(m, s, m2, s2);
+  }
+  if (lane == 0) {
+    sm.red_m[warp] = (double)m;
+    sm.red_s[warp] = (double)s;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double M = sm.red_m[0], S = sm.red_s[0];
+    for (int w = 1; w < kConsumerWarps; ++w) {
+      const double m2 = sm.red_m[w], s2 = sm.red_s[w];
+      if (m2 == -INFINITY) continue;
+      if (m2 > M) {
+        S = (M == -INFINITY ? 0.0 : S * exp(M - m2)) + s2;
+        M = m2;
+      } else {
+        S += s2 * exp(m2 - M);
+      }
+    }
+    PosEval ev;
+    ev.mt = M;
+    ev.lst = log(S);
+    ev.md = ev.lsd = ev.lsz = 0.0;
+    set_weigher(wf, kWeightPlain, ev, (double)p.omt_f, (double)p.tau_f);
+  }
+  __syncthreads();
+  const double u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b, (uint32_t)j);
+  int near = 0;
+  const int idx = cdf_sample<In, Acc>(rd, rd, wf, p.vocab_local, u, p.eps_u, &sm.samp, tid, &near);
+  if (tid == 0) tokens[row] = idx < 0 ? -1 : p.vocab_offset + idx;
+}
+
+// ------------------------------------------------------------------ synth
+__device__ __forceinline__ float u01_open(uint32_t x) {
+  return ((float)(x >> 8) + 0.5f) * (1.0f / 16777216.0f);  // (0, 1)
+}
+
+__device__ __forceinline__ unsigned gcd_u(unsigned a, unsigned b) {
+  while (b) {
+    const unsigned t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+template <class Out>
+__device__ __forceinline__ Out to_out(float x);
+template <>
+__device__ __forceinline__ float to_out<float>(float x) {
+  return x;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+// Families by b mod 4: Zipf target l_t[i] = -sigma ln(1 + pi(i)),
+// pi(i) = (a i + c) mod V with gcd(a, V) = 1, sigma 1.2 / 2.5 / 3.5; Gaussian
+// target sigma 6. Draft = target + delta N(0, 1), delta 0.8 / 1.0 / 1.5 / 2.
+template <class Out>
+__global__ void __launch_bounds__(256)
+    synth_logits_kernel(int B, int gamma, int V, int stride, uint64_t seed, Out *__restrict__ draft,
+                        Out *__restrict__ target) {
+  const int G1 = gamma + 1;
+  const int item = blockIdx.x;  // b * (gamma + 1) + j
+  const int b = item / G1, j = item - b * G1;
+  const int fam = b & 3;
+  const float sigma_tab[4] = {1.2f, 2.5f, 3.5f, 6.0f};
+  const float delta_tab[4] = {0.8f, 1.0f, 1.5f, 2.0f};
+  const float sigma = sigma_tab[fam], delta = delta_tab[fam];
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const dsdv_philox_out rp = dsdv_philox4x32_10(0xffffffffu, (uint32_t)item, 0x5eedu, 0u, k0, k1);
+  unsigned a = 1u + 2u * (rp.v[0] % (unsigned)(V / 2 > 0 ? V / 2 : 1));
+  while (gcd_u(a % (unsigned)V, (unsigned)V) != 1u) a += 2u;
+  a %= (unsigned)V;
+  const unsigned c = rp.v[1] % (unsigned)V;
+  Out *rt = target + (size_t)item * stride;
+  Out *rd = (j < gamma) ? draft + ((size_t)b * gamma + j) * stride : nullptr;
+  const Out ninf = to_out<Out>(-INFINITY);
+  for (int i = threadIdx.x; i < stride; i += blockDim.x) {
+    if (i >= V) {
+      rt[i] = ninf;
+      if (rd) rd[i] = ninf;
+      continue;
+    }
+    const dsdv_philox_out r = dsdv_philox4x32_10((uint32_t)i, (uint32_t)item, 0x10917u, 0u, k0, k1);
+    const float r1 = sqrtf(-2.0f * logf(u01_open(r.v[0])));
+    const float th = 6.283185307179586f * u01_open(r.v[1]);
+    const float z0 = r1 * cosf(th), z1 = r1 * sinf(th);
+    float lt;
+    if (fam < 3) {
+      const unsigned pi = (unsigned)(((unsigned long long)a * (unsigned)i + c) % (unsigned)V);
+      lt = -sigma * logf(1.0f + (float)pi);
+    } else {
+      lt = sigma * z0;
+    }
+    // round the target first so that draft = stored target + noise
+    const Out lt_o = to_out<Out>(lt);
+    rt[i] = lt_o;
+    if (rd) {
+      const float ltr = (float)lt_o;
+      rd[i] = to_out<Out>(ltr + delta * z1);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launch
+template <class In>
+cudaError_t launch_sample_extra(const DevParams &p, const void *draft, const void *target,
+                                const double *records, const int32_t *position,
+                                const double *uniform, int32_t *token_out, int32_t *status,
+                                cudaStream_t stream) {
+  sample_extra_kernel<In><<<p.B, kConsumerThreads, 0, stream>>>(
+      p, (const In *)draft, (const In *)target, records, position, uniform, token_out, status);
+  return cudaGetLastError();
+}
+
+template <class In>
+cudaError_t launch_draft_sample(const DevParams &p, const void *draft, int32_t *tokens,
+                                cudaStream_t stream) {
+  draft_sample_kernel<In><<<p.B * p.gamma, kConsumerThreads, 0, stream>>>(p, (const In *)draft,
+                                                                          tokens);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth(int dtype, int B, int gamma, int V, int stride, uint64_t seed, void *draft,
+                         void *target, cudaStream_t stream) {
+  const int grid = B * (gamma + 1);
+  if (dtype == DSDV_DTYPE_BF16)
+    synth_logits_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>(
+        B, gamma, V, stride, seed, (__nv_bfloat16 *)draft, (__nv_bfloat16 *)target);
+  else
+    synth_logits_kernel<float><<<grid, 256, 0, stream>>>(B, gamma, V, stride, seed, (float *)draft,
+                                                          (float *)target);
+  return cudaGetLastError();
+}
+
+#define DSDV_INST(T)                                                                             \
+  template cudaError_t launch_sample_extra<T>(const DevParams &, const void *, const void *,     \
+                                              const double *, const int32_t *, const double *,  \
+                                              int32_t *, int32_t *, cudaStream_t);               \
+  template cudaError_t launch_draft_sample<T>(const DevParams &, const void *, int32_t *,        \
+                                              cudaStream_t);
+DSDV_INST(__nv_bfloat16)
+DSDV_INST(float)
+DSDV_INST(double)
+#undef DSDV_INST
+
+}  // namespace dsdv

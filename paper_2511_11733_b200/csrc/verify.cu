@@ -1,0 +1,1237 @@
+// Fused adaptive speculative verification for sm_100a (DSD, arXiv 2511.11733).
+//
+// One persistent, warp-specialised kernel (one CTA per SM) verifies a whole
+// window for all B sequences. Work items are claimed from a global ticket in
+// position-major order:
+//   (b, j < gamma): the row pair (draft row j, target row j)
+//   (b, gamma)    : target row gamma (bonus draw)
+//
+// Warp roles inside a CTA:
+//   producer  (1 warp)  streams rows through a kStages-deep shared-memory ring
+//                       with 1-D bulk copies (TMA engine, mbarrier completion);
+//   compute   (16 warps) fold every 16-byte vector into per-thread online
+//                       statistics — (max, sum exp) of l_t, l_d and of the
+//                       softened mix (1-tau) l_t + tau l_d (soften,
+//                       verifier.cpp:161-186, as a third accumulator sharing the
+//                       row exponents), warp top-m lists of l_t and l_d in
+//                       (value desc, id asc) order (top_ids, verifier.cpp:40-51;
+//                       softmax is monotone so logit order is probability
+//                       order) behind a one-compare threshold filter, and a
+//                       bitwise row-equality flag (soften's short-circuit,
+//                       verifier.cpp:172) — and at the end of an item publish a
+//                       per-warp partial record into one of kSlots slots
+//                       without ever waiting for the epilogue;
+//   epilogue  (1 warp)  merges the partials, evaluates token_cross_entropy
+//                       (:112-117), norm_match (:119-134), is_key (:136-159),
+//                       the effective distribution (:231-233) and accept_prob
+//                       (:188-196) in fp64, draws the Philox accept uniform and
+//                       publishes a per-position flag.
+//
+// The extra draw (residual of a rejected position, :198-213, :245-246, or the
+// bonus draw, :253-256) is needed by a position whose predecessors are not
+// already known to have stopped the window. The epilogue posts it back to the
+// producer as a "sample item": the rows are streamed again (L2-resident) and
+// the compute warps turn them into per-tile sums of the residual / bonus
+// weights; the epilogue then scans the tile sums for u * W and resolves the
+// crossing tile (sample_with_uniform, distribution.cpp:103-114). The last item
+// of a sequence to finish (per-sequence counter) commits the round: first
+// rejection (:223-250), k, extra token, key count.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "sample.cuh"
+
+namespace dsdv {
+namespace fz {
+
+constexpr int kCW = 16;              // compute warps
+constexpr int kCT = kCW * 32;        // compute threads
+constexpr int kEW = 2;               // epilogue warps (alternate stream items)
+constexpr int kEpiWarp = kCW;        // first epilogue warp index
+constexpr int kProdWarp = kCW + kEW; // producer warp index
+constexpr int kThreads = (kCW + kEW + 1) * 32;
+constexpr int kRowBytes = 16384;     // per row per ring stage
+constexpr int kVecs = kRowBytes / 16 / kCT;  // 16-byte vectors per compute thread per row (4)
+constexpr int kStages = 4;
+constexpr int kSlots = 4;
+constexpr int kMaxTiles = 2048;      // blocks per slot: (chunk, vector, warp), 32*VEC ids each
+constexpr int kReq = 16;             // sample-request queue
+constexpr float kSlack = 8.0f;       // lazy max: rescale when a value exceeds m by this much
+constexpr float kFloorM = -1e30f;    // finite "empty" max (keeps (v - m) free of inf - inf)
+
+enum ItemKind : int { kRegular = 0, kSample = 1 };
+
+struct StageMeta {
+  int item;   // global item id (b, j), -1 = end of stream
+  int chunk;
+  int kind;   // kRegular / kSample
+  int n;      // CTA-local stream index (slot = n % kSlots)
+  int req;    // sample request index
+};
+
+template <class Acc>
+struct WarpPartial {
+  Acc mt, st, md, sd, sz;
+  int diff;
+};
+
+template <class Acc>
+struct Slot {
+  int item;
+  int kind;
+  int req;
+  WarpPartial<Acc> wp[kCW];
+  union {
+    int bmax[2][kMaxTiles];  // regular item: per-block max keys of l_t / l_d (top-m candidates)
+    double tiles[kMaxTiles];  // sample item: per-block weight sums
+  } u;
+};
+
+template <class Acc>
+struct Request {
+  int ready;  // set by the epilogue once the entry is complete
+  int item;
+  int rows;   // 2 = row pair (residual), 1 = target row (bonus)
+  double u;
+  Weigher<Acc> wf;
+};
+
+template <class Acc>
+struct alignas(128) Smem {
+  uint8_t ring[kStages][2][kRowBytes];  // [stage][0 = draft, 1 = target]
+  Slot<Acc> slot[kSlots];
+  Request<Acc> req[kReq];
+  StageMeta meta[kStages];
+  uint64_t full[kStages], empty[kStages];
+  uint64_t part_full[kSlots], part_empty[kSlots];
+  int req_head;            // producer: next request to stream
+  int req_tail;            // epilogue warps: next request entry to fill (atomic)
+  int req_done;            // sample items finished (entries free again)
+  int epi_count;           // stream items the epilogue warps have finished
+  int epi_exit;            // epilogue warps that have left
+  int cand[kEW][32];       // epilogue scratch: candidate blocks of a batch
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ bool bits_differ(float a, float b) {
+  return __float_as_uint(a) != __float_as_uint(b);
+}
+__device__ __forceinline__ bool bits_differ(double a, double b) {
+  return __double_as_longlong(a) != __double_as_longlong(b);
+}
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
+
+// Order-preserving int key of a float (shared-memory atomicMax of thresholds).
+__device__ __forceinline__ int fkey(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+// doubles round DOWN so the key stays a lower bound of the true threshold
+__device__ __forceinline__ int fkey(double f) { return fkey(__double2float_rd(f)); }
+__device__ __forceinline__ float fkey_inv(int k) {
+  return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff);
+}
+constexpr int kKeyNegInf = (int)(0xff800000u ^ 0x7fffffffu);  // fkey(-inf)
+
+__device__ __forceinline__ int vload(const int *p) { return *(const volatile int *)p; }
+__device__ __forceinline__ void vstore(int *p, int v) { *(volatile int *)p = v; }
+
+template <class Acc>
+struct ItemState {
+  Acc mt, st, md, sd, sz;
+  uint32_t diff;
+  __device__ __forceinline__ void reset() {
+    mt = md = Acc(kFloorM);
+    st = sd = sz = Acc(0);
+    diff = 0;
+  }
+};
+
+__device__ __forceinline__ int warp_max_key(int key) {
+  int r;
+  asm volatile("redux.sync.max.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(key));
+  return r;
+}
+
+// ------------------------------------------------------------------ compute warps
+// Exponent sums of one vector (hot path). fp32: packed f32x2 arithmetic, the
+// softened-mix exponent on the FMA-pipe polynomial (MUFU keeps t and d).
+template <bool PAIR, bool NEEDZ, int VEC>
+__device__ __forceinline__ void exp_sums(const float (&vt)[VEC], const float (&vd)[VEC],
+                                         ItemState<float> &S, const DevParams &p) {
+  const f32x2 L2 = pk2(kLog2eF, kLog2eF);
+  const f32x2 mt2 = pk2(S.mt, S.mt), md2 = pk2(S.md, S.md);
+  const f32x2 omt2 = pk2(p.omt_f, p.omt_f), tau2 = pk2(p.tau_f, p.tau_f);
+  f32x2 at = pk2(0.f, 0.f), ad = pk2(0.f, 0.f), az = pk2(0.f, 0.f);
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    const f32x2 xt = mul2(sub2(pk2(vt[e], vt[e + 1]), mt2), L2);
+    at = add2(at, pk2(fast_exp2(lo2(xt)), fast_exp2(hi2(xt))));
+    if (PAIR) {
+      const f32x2 xd = mul2(sub2(pk2(vd[e], vd[e + 1]), md2), L2);
+      ad = add2(ad, pk2(fast_exp2(lo2(xd)), fast_exp2(hi2(xd))));
+      if (NEEDZ) az = add2(az, poly_exp2x2(fma2(omt2, xt, mul2(tau2, xd))));
+    }
+  }
+  S.st += lo2(at) + hi2(at);
+  if (PAIR) {
+    S.sd += lo2(ad) + hi2(ad);
+    if (NEEDZ) S.sz += lo2(az) + hi2(az);
+  }
+}
+
+template <bool PAIR, bool NEEDZ, int VEC>
+__device__ __forceinline__ void exp_sums(const double (&vt)[VEC], const double (&vd)[VEC],
+                                         ItemState<double> &S, const DevParams &p) {
+  const double L = kLog2e, omt = (double)p.omt_f, tau = (double)p.tau_f;
+  double at = 0.0, ad = 0.0, az = 0.0;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    const double xt = (vt[e] - S.mt) * L;
+    at += exp2(xt);
+    if (PAIR) {
+      const double xd = (vd[e] - S.md) * L;
+      ad += exp2(xd);
+      if (NEEDZ) az += exp2(omt * xt + tau * xd);
+    }
+  }
+  S.st += at;
+  if (PAIR) {
+    S.sd += ad;
+    if (NEEDZ) S.sz += az;
+  }
+}
+
+// Fold one 16-byte vector per row (ids id0..id0+VEC-1; block bi). Top-m
+// bookkeeping is one warp max per vector and row (REDUX) stored as the
+// block's key: the epilogue selects the exact top-m from the few blocks whose
+// maxima can reach it. The only control flow is the warp vote of the (rare)
+// lazy rescale. Called from a rolled loop: the hot loop stays small enough
+// for the instruction caches.
+template <class In, bool PAIR, bool NEEDZ>
+__device__ __forceinline__ void fold_vec(const uint8_t *sdraft, const uint8_t *starget, int q,
+                                         int id0, bool tail, ItemState<typename InTraits<In>::Acc> &S,
+                                         const DevParams &p, int lane, int bi, int *bmax_t,
+                                         int *bmax_d) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int VEC = InTraits<In>::kVec;
+  const Acc L = log2e<Acc>();
+  const Acc ni = neg_inf<Acc>();
+
+  Acc vt[VEC], vd[VEC];
+  const uint4 a = lds128(starget + q * 16);
+  unpack(a, vt, (In *)nullptr);
+  uint32_t diff = 0;
+  if (PAIR) {
+    const uint4 bb = lds128(sdraft + q * 16);
+    unpack(bb, vd, (In *)nullptr);
+    diff = (a.x ^ bb.x) | (a.y ^ bb.y) | (a.z ^ bb.z) | (a.w ^ bb.w);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) vd[e] = Acc(0);
+  }
+  if (tail) {
+    // elements past the logical row are -inf in both rows (no mass, equal,
+    // ranked after every real id); the equality flag sees real ids only
+    diff = 0;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      if (id0 + e >= p.vocab_local) {
+        vt[e] = ni;
+        if (PAIR) vd[e] = ni;
+      } else if (PAIR) {
+        diff |= bits_differ(vt[e], vd[e]) ? 1u : 0u;
+      }
+    }
+  }
+  Acc cmt = vt[0];
+#pragma unroll
+  for (int e = 1; e < VEC; ++e) cmt = vmax(cmt, vt[e]);
+  Acc cmd = ni;
+  if (PAIR) {
+    S.diff |= diff;
+    cmd = vd[0];
+#pragma unroll
+    for (int e = 1; e < VEC; ++e) cmd = vmax(cmd, vd[e]);
+    const int bt = warp_max_key(fkey(cmt));
+    const int bd = warp_max_key(fkey(cmd));
+    if (lane == 0) {
+      bmax_t[bi] = bt;
+      bmax_d[bi] = bd;
+    }
+  }
+  // lazy online max: one warp vote, rarely taken
+  const bool up_t = cmt > S.mt + Acc(kSlack);
+  const bool up_d = PAIR && (cmd > S.md + Acc(kSlack));
+  if (__any_sync(0xffffffffu, up_t || up_d)) {
+    const Acc nt = up_t ? cmt : S.mt;
+    const Acc nd = up_d ? cmd : S.md;
+    if (NEEDZ) S.sz *= fast_exp2((Acc(p.omt_f) * (S.mt - nt) + Acc(p.tau_f) * (S.md - nd)) * L);
+    S.st *= fast_exp2((S.mt - nt) * L);
+    if (PAIR) S.sd *= fast_exp2((S.md - nd) * L);
+    S.mt = nt;
+    S.md = nd;
+  }
+  exp_sums<PAIR, NEEDZ, VEC>(vt, vd, S, p);
+}
+
+// Sample item: per-tile fp64 sums of the residual / bonus weights. Tile
+// (chunk, h, warp) covers ids [chunk*CH + (h*kCT + warp*32)*VEC, +32*VEC):
+// tile index order is id order.
+template <class In>
+__device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_t *starget,
+                                             int chunk, const Weigher<typename InTraits<In>::Acc> &wf,
+                                             double *tiles, const DevParams &p, int tid, int warp,
+                                             int lane) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int VEC = InTraits<In>::kVec;
+  constexpr int CH = kRowBytes / (int)sizeof(In);
+#pragma unroll
+  for (int h = 0; h < kVecs; ++h) {
+    const int q = h * kCT + tid;
+    const int id0 = chunk * CH + q * VEC;
+    Acc vt[VEC], vd[VEC];
+    unpack(lds128(starget + q * 16), vt, (In *)nullptr);
+    if (wf.kind != kWeightPlain) {
+      unpack(lds128(sdraft + q * 16), vd, (In *)nullptr);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) vd[e] = Acc(0);
+    }
+    Acc ls = Acc(0);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const Acc w = (id0 + e < p.vocab_local) ? wf(vt[e], vd[e]) : Acc(0);
+      ls = add_rn(ls, w);
+    }
+    const double ts = warp_sum_f64((double)ls);
+    if (lane == 0) tiles[(chunk * kVecs + h) * kCW + warp] = ts;
+  }
+}
+
+template <class In, bool NEEDZ>
+__device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p, int tid) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int VEC = InTraits<In>::kVec;
+  constexpr int CH = kRowBytes / (int)sizeof(In);
+  const int warp = tid >> 5, lane = tid & 31;
+  ItemState<Acc> S;
+  S.reset();
+  int stage = 0;
+  uint32_t phase = 0;
+  bool pair = false;
+  int kind = kRegular, n = 0, s = 0;
+  for (;;) {
+    mbar_wait(&sm.full[stage], phase);
+    const StageMeta md = sm.meta[stage];
+    if (md.item < 0) {
+      // end of stream: one terminating slot per epilogue warp
+      for (int k = 0; k < kEW; ++k) {
+        const int nn = md.n + k, ns = nn % kSlots;
+        mbar_wait(&sm.part_empty[ns], ((nn / kSlots) & 1) ^ 1);
+        if (tid == 0) sm.slot[ns].item = -1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.part_full[ns]);
+      }
+      break;
+    }
+    const int c = md.chunk;
+    if (c == 0) {
+      kind = md.kind;
+      n = md.n;
+      s = n % kSlots;
+      const int j = md.item / p.B;
+      pair = j < p.gamma;
+      // the slot (partials + thresholds) must be free before this item runs
+      mbar_wait(&sm.part_empty[s], ((n / kSlots) & 1) ^ 1);
+    }
+    const bool last = c == p.n_chunks - 1;
+    if (kind == kRegular) {
+      const bool tail = last && (p.vocab_local % CH) != 0;
+      int *bt = sm.slot[s].u.bmax[0];
+      int *bd = sm.slot[s].u.bmax[1];
+      if (pair) {
+#pragma unroll 1
+        for (int h = 0; h < kVecs; ++h) {
+          const int q = h * kCT + tid;
+          fold_vec<In, true, NEEDZ>(sm.ring[stage][0], sm.ring[stage][1], q, c * CH + q * VEC,
+                                    tail, S, p, lane, (c * kVecs + h) * kCW + warp, bt, bd);
+        }
+      } else {
+#pragma unroll 1
+        for (int h = 0; h < kVecs; ++h) {
+          const int q = h * kCT + tid;
+          fold_vec<In, false, false>(sm.ring[stage][0], sm.ring[stage][1], q, c * CH + q * VEC,
+                                     tail, S, p, lane, 0, bt, bd);
+        }
+      }
+    } else {
+      sample_chunk<In>(sm.ring[stage][0], sm.ring[stage][1], c, sm.req[md.req].wf,
+                       sm.slot[s].u.tiles, p, tid, warp, lane);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+    if (!last) continue;
+
+    // ---- item end: publish this warp's partial, never wait for the epilogue ----
+    Slot<Acc> &sl = sm.slot[s];
+    if (kind == kRegular) {
+      const Acc omt = Acc(p.omt_f), tau = Acc(p.tau_f), L = log2e<Acc>();
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const Acc mt2 = __shfl_xor_sync(0xffffffffu, S.mt, off);
+        const Acc st2 = __shfl_xor_sync(0xffffffffu, S.st, off);
+        const Acc md2 = __shfl_xor_sync(0xffffffffu, S.md, off);
+        const Acc sd2 = __shfl_xor_sync(0xffffffffu, S.sd, off);
+        const Acc sz2 = __shfl_xor_sync(0xffffffffu, S.sz, off);
+        const Acc Mn = vmax(S.mt, mt2), Dn = vmax(S.md, md2);
+        S.st = S.st * fast_exp2((S.mt - Mn) * L) + st2 * fast_exp2((mt2 - Mn) * L);
+        S.sd = S.sd * fast_exp2((S.md - Dn) * L) + sd2 * fast_exp2((md2 - Dn) * L);
+        S.sz = S.sz * fast_exp2((omt * (S.mt - Mn) + tau * (S.md - Dn)) * L) +
+               sz2 * fast_exp2((omt * (mt2 - Mn) + tau * (md2 - Dn)) * L);
+        S.mt = Mn;
+        S.md = Dn;
+      }
+      const int anydiff = __any_sync(0xffffffffu, S.diff != 0);
+      if (lane == 0) {
+        WarpPartial<Acc> w;
+        w.mt = S.mt;
+        w.st = S.st;
+        w.md = S.md;
+        w.sd = S.sd;
+        w.sz = S.sz;
+        w.diff = anydiff;
+        sl.wp[warp] = w;
+      }
+      S.reset();
+    }
+    if (tid == 0) {
+      sl.item = md.item;
+      sl.kind = kind;
+      sl.req = md.req;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.part_full[s]);
+  }
+}
+
+// ------------------------------------------------------------------ epilogue warp
+// fp64 merge of the kCW warp partials (lanes 0..kCW-1, xor tree).
+template <class Acc>
+__device__ __noinline__ void merge_partials(const Slot<Acc> &sl, const DevParams &p, int lane,
+                                               double (&out)[5], int &diff) {
+  double mt = -INFINITY, st = 0.0, md = -INFINITY, sd = 0.0, sz = 0.0;
+  int df = 0;
+  if (lane < kCW) {
+    const WarpPartial<Acc> w = sl.wp[lane];
+    mt = (double)w.mt;
+    st = (double)w.st;
+    md = (double)w.md;
+    sd = (double)w.sd;
+    sz = (double)w.sz;
+    df = w.diff;
+  }
+  const double omt = (double)p.omt_f, tau = (double)p.tau_f;
+#pragma unroll 1
+  for (int off = 16; off > 0; off >>= 1) {
+    const double mt2 = __shfl_xor_sync(0xffffffffu, mt, off);
+    const double st2 = __shfl_xor_sync(0xffffffffu, st, off);
+    const double md2 = __shfl_xor_sync(0xffffffffu, md, off);
+    const double sd2 = __shfl_xor_sync(0xffffffffu, sd, off);
+    const double sz2 = __shfl_xor_sync(0xffffffffu, sz, off);
+    df |= __shfl_xor_sync(0xffffffffu, df, off);
+    const double Mn = fmax(mt, mt2), Dn = fmax(md, md2);
+    sz = (sz != 0.0 ? sz * exp(omt * (mt - Mn) + tau * (md - Dn)) : 0.0) +
+         (sz2 != 0.0 ? sz2 * exp(omt * (mt2 - Mn) + tau * (md2 - Dn)) : 0.0);
+    st = (st != 0.0 ? st * exp(mt - Mn) : 0.0) + (st2 != 0.0 ? st2 * exp(mt2 - Mn) : 0.0);
+    sd = (sd != 0.0 ? sd * exp(md - Dn) : 0.0) + (sd2 != 0.0 ? sd2 * exp(md2 - Dn) : 0.0);
+    mt = Mn;
+    md = Dn;
+  }
+  out[0] = mt;
+  out[1] = st;
+  out[2] = md;
+  out[3] = sd;
+  out[4] = sz;
+  diff = df;
+}
+
+// Key list: the same warp-distributed sorted list as TopList, over int keys.
+struct KeyList {
+  int v, id, theta;
+  __device__ __forceinline__ void reset() {
+    v = INT_MIN;
+    id = 0x7fffffff;
+    theta = INT_MIN;
+  }
+  __device__ __forceinline__ bool full(int M) const {
+    return __shfl_sync(0xffffffffu, id, M - 1) != 0x7fffffff;
+  }
+  __device__ __forceinline__ void insert(int cv, int cid, int M, int lane) {
+    const bool beats = lane < M && (v > cv || (v == cv && id < cid));
+    const int pos = __popc(__ballot_sync(0xffffffffu, beats));
+    if (pos < M) {
+      const int uv = __shfl_up_sync(0xffffffffu, v, 1);
+      const int ui = __shfl_up_sync(0xffffffffu, id, 1);
+      if (lane > pos && lane < M) {
+        v = uv;
+        id = ui;
+      }
+      if (lane == pos) {
+        v = cv;
+        id = cid;
+      }
+      theta = __shfl_sync(0xffffffffu, v, M - 1);
+    }
+  }
+};
+
+// Exact top-M of one row, (value desc, id asc) like top_ids (verifier.cpp:40-51),
+// from the per-block maxima the compute warps recorded. theta_b, the M-th
+// largest block maximum, is at most the row's M-th value (the M largest block
+// maxima are M distinct elements), so only blocks whose maximum reaches it
+// and, inside them, only elements >= theta_b can belong to the top M. Those
+// blocks are re-read (L2-resident) and their survivors inserted. Ids past the
+// logical row (ragged-tail padding) never enter.
+template <class In>
+__device__ __noinline__ TopList<typename InTraits<In>::Acc> select_topm(const int *bmax, int nblocks,
+                                                           const In *row, int M, int nlocal,
+                                                           int *cand, int lane) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int VEC = InTraits<In>::kVec;
+  constexpr int CH = kRowBytes / (int)sizeof(In);
+  KeyList K;
+  K.reset();
+  for (int base = 0; base < nblocks; base += 32) {
+    const int bi = base + lane;
+    const int key = bi < nblocks ? bmax[bi] : INT_MIN;
+    unsigned q = __ballot_sync(0xffffffffu, bi < nblocks && key >= K.theta);
+    while (q) {
+      const int src = __ffs(q) - 1;
+      q &= q - 1;
+      const int cv = __shfl_sync(0xffffffffu, key, src);
+      if (cv >= K.theta) K.insert(cv, base + src, M, lane);
+    }
+  }
+  const int theta_b = K.full(M) ? K.theta : INT_MIN;
+  const Acc vb = (Acc)fkey_inv(theta_b);
+  TopList<Acc> L;
+  L.reset();
+  for (int base = 0; base < nblocks; base += 32) {
+    const int bi = base + lane;
+    const bool c = bi < nblocks && bmax[bi] >= theta_b;
+    unsigned q = __ballot_sync(0xffffffffu, c);
+    // gather this batch's candidate blocks, then re-read them 4 at a time
+    int nc = 0;
+    while (q) {
+      const int src = __ffs(q) - 1;
+      q &= q - 1;
+      if (lane == 0) cand[nc] = base + src;
+      ++nc;
+    }
+    __syncwarp();
+    for (int g = 0; g < nc; g += 4) {
+      uint4 raw[4];
+      int id0[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        id0[k] = -1;
+        raw[k] = make_uint4(0, 0, 0, 0);
+        if (g + k < nc) {
+          const int b = cand[g + k];
+          const int cc = b / (kVecs * kCW), r = b - cc * kVecs * kCW;
+          const int h = r / kCW, w = r - h * kCW;
+          id0[k] = cc * CH + (h * kCT + w * 32 + lane) * VEC;
+          if (id0[k] < nlocal) raw[k] = ldg128(row + id0[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (g + k >= nc) break;
+        Acc v[VEC];
+        unpack(raw[k], v, (In *)nullptr);
+        unsigned qm = 0;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          if (id0[k] + e < nlocal && v[e] >= vb && v[e] >= L.theta) qm |= 1u << e;
+        unsigned lanes = __ballot_sync(0xffffffffu, qm != 0);
+        while (lanes) {
+          const int src = __ffs(lanes) - 1;
+          lanes &= lanes - 1;
+          unsigned m = __shfl_sync(0xffffffffu, qm, src);
+          const int ib = __shfl_sync(0xffffffffu, id0[k], src);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const Acc cv = __shfl_sync(0xffffffffu, v[e], src);
+            if (((m >> e) & 1u) && cv >= L.theta) L.insert(cv, ib + e, M, lane);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  return L;
+}
+
+// Exact log-sum-exp of the softened mix (two fp64 passes, one warp) for the
+// rare rows whose online mix sum underflowed against its reference point.
+template <class In>
+__device__ __noinline__ double exact_lse_mix_warp(const In *rt, const In *rd, int n, double omt,
+                                                  double tau, int lane) {
+  constexpr int VEC = InTraits<In>::kVec;
+  using Acc = typename InTraits<In>::Acc;
+  const int nvec = (n + VEC - 1) / VEC;
+  double zmax = -INFINITY;
+  for (int q = lane; q < nvec; q += 32) {
+    Acc t[VEC], d[VEC];
+    unpack(ldg128(rt + q * VEC), t, (In *)nullptr);
+    unpack(ldg128(rd + q * VEC), d, (In *)nullptr);
+    for (int e = 0; e < VEC; ++e)
+      if (q * VEC + e < n) zmax = fmax(zmax, omt * (double)t[e] + tau * (double)d[e]);
+  }
+  for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+  if (zmax == -INFINITY) return -INFINITY;
+  double s = 0.0;
+  for (int q = lane; q < nvec; q += 32) {
+    Acc t[VEC], d[VEC];
+    unpack(ldg128(rt + q * VEC), t, (In *)nullptr);
+    unpack(ldg128(rd + q * VEC), d, (In *)nullptr);
+    for (int e = 0; e < VEC; ++e)
+      if (q * VEC + e < n) s += exp(omt * (double)t[e] + tau * (double)d[e] - zmax);
+  }
+  s = warp_sum_f64(s);
+  return zmax + log(s);
+}
+
+// Lane 0: evaluate one position from merged statistics (token_cross_entropy
+// :112-117, norm_match :119-134, is_key :136-159, effective distribution
+// :231-233 with soften's short-circuits :170-172).
+template <class In>
+__device__ __noinline__ void evaluate_position(const double (&mrg)[5], int diff, int shared,
+                                               const DevParams &p, const In *rt, const In *rd,
+                                               int y, bool pair, PosEval &ev) {
+  const double Mt = mrg[0], St = mrg[1], Md = mrg[2], Sd = mrg[3], Sz = mrg[4];
+  ev.mt = Mt;
+  ev.lst = log(St);
+  ev.md = Md;
+  ev.lsd = pair ? log(Sd) : 0.0;
+  ev.lsz = 0.0;
+  ev.err = 0;
+  ev.key = 0;
+  ev.kind = DSDV_EFF_TARGET;
+  ev.near = 0;
+  ev.need_exact = 0;
+  ev.accepted = 0;
+  ev.h_t = ev.h_d = ev.p_t_y = ev.p_d_y = ev.nm = ev.p_eff = ev.a = ev.u = 0.0;
+  ev.lt_y = ev.ld_y = -INFINITY;
+  // Distribution invariants (distribution.cpp:29-63): finite, positive mass.
+  if (!(St > 0.0 && isfinite(St))) ev.err = DSDV_E_INVARIANT;
+  if (!pair) return;
+  if (!(Sd > 0.0 && isfinite(Sd)) && !ev.err) ev.err = DSDV_E_INVARIANT;
+  // check_token_in_vocab (verifier.cpp:32-37)
+  const int yl = y - p.vocab_offset;
+  const bool y_ok = y >= 0 && y < p.V && yl >= 0 && yl < p.vocab_local;
+  if (!y_ok && !ev.err) ev.err = DSDV_E_INVARIANT;
+  if (y_ok) {
+    ev.lt_y = load_scalar<In>(rt + yl);
+    ev.ld_y = load_scalar<In>(rd + yl);
+  }
+  const double lse_t = Mt + ev.lst, lse_d = Md + ev.lsd;
+  ev.h_t = (ev.lt_y == -INFINITY) ? INFINITY : lse_t - ev.lt_y;
+  ev.h_d = (ev.ld_y == -INFINITY) ? INFINITY : lse_d - ev.ld_y;
+  ev.p_t_y = exp(ev.lt_y - lse_t);
+  ev.p_d_y = exp(ev.ld_y - lse_d);
+  const bool certain = ev.h_t < kCertainSurprisal;
+  const bool ratio_cert = ev.h_d > 0.0;
+  const bool ratio_rel = ev.h_d / ev.h_t > p.ratio_limit;
+  const bool ratio = certain ? ratio_cert : ratio_rel;
+  const double gap = fabs(ev.p_t_y - ev.p_d_y);
+  const bool gapc = gap > p.gap_limit;
+  ev.nm = (double)shared / (double)p.top_m;
+  const bool overlap = ev.nm < p.overlap_floor;
+  ev.key = (ratio || gapc || overlap) ? 1 : 0;
+  // near-threshold bookkeeping (fp32 statistics vs the fp64 reference)
+  const double el = p.eps_lambda;
+  if (ev.h_t < 1e-6 && (ratio_cert != ratio_rel || ev.h_d < 1e-6)) ev.near = 1;
+  if (isfinite(p.ratio_limit) && ev.h_t >= 1e-6 && isfinite(ev.h_d) &&
+      fabs(ev.h_d / ev.h_t - p.ratio_limit) < el * fmax(1.0, p.ratio_limit))
+    ev.near = 1;
+  if (fabs(gap - p.gap_limit) < el * fmax(1.0, p.gap_limit)) ev.near = 1;
+  if (ev.key || p.tau == 0.0 || diff == 0)
+    ev.kind = DSDV_EFF_TARGET;
+  else if (p.tau == 1.0)
+    ev.kind = DSDV_EFF_DRAFT;
+  else
+    ev.kind = DSDV_EFF_SOFTENED;
+  if (ev.kind == DSDV_EFF_SOFTENED && !ev.err) {
+    if (Sz > 1e-30 && isfinite(Sz))
+      ev.lsz = log(Sz);
+    else
+      ev.need_exact = 1;
+  }
+}
+
+// Lane 0: effective probability at y, accept_prob (verifier.cpp:188-196) and
+// the strict accept test u < a (:237).
+__device__ __forceinline__ void decide_position(const DevParams &p, int b, int j, PosEval &ev) {
+  double p_eff = ev.p_t_y;
+  if (ev.kind == DSDV_EFF_DRAFT) p_eff = ev.p_d_y;
+  if (ev.kind == DSDV_EFF_SOFTENED && !ev.err) {
+    const double lse_z = (double)p.omt_f * ev.mt + (double)p.tau_f * ev.md + ev.lsz;
+    const double z_y = (1.0 - p.tau) * ev.lt_y + p.tau * ev.ld_y;
+    p_eff = exp(z_y - lse_z);
+  }
+  if (!ev.err && !(ev.p_d_y > 0.0)) ev.err = DSDV_E_DRAFTING_CONTRACT;
+  ev.p_eff = p_eff;
+  ev.a = ev.err ? 0.0 : fmin(1.0, p_eff / ev.p_d_y);
+  ev.u = 0.0;
+  ev.accepted = 0;
+  if (!p.stats_only) {
+    ev.u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b,
+                               (uint32_t)(p.gamma + j));
+    ev.accepted = (!ev.err && ev.u < ev.a) ? 1 : 0;
+    if (!ev.err && fabs(ev.u - ev.a) < p.eps_u) ev.near = 1;
+  }
+}
+
+__device__ __forceinline__ void write_position(const DevOut &o, const DevParams &p, int b, int j,
+                                               bool pair, const PosEval &ev) {
+  const int G1 = p.gamma + 1;
+  if (pair) {
+    const size_t pos = (size_t)b * p.gamma + j;
+    if (o.key_mask) o.key_mask[pos] = (uint8_t)ev.key;
+    if (o.accepted) o.accepted[pos] = (uint8_t)ev.accepted;
+    if (o.accept_prob) o.accept_prob[pos] = ev.a;
+    if (o.h_target) o.h_target[pos] = ev.h_t;
+    if (o.h_draft) o.h_draft[pos] = ev.h_d;
+    if (o.p_target_y) o.p_target_y[pos] = ev.p_t_y;
+    if (o.p_draft_y) o.p_draft_y[pos] = ev.p_d_y;
+    if (o.norm_match) o.norm_match[pos] = ev.nm;
+    if (o.p_effective_y) o.p_effective_y[pos] = ev.p_eff;
+    if (o.uniform) o.uniform[pos] = ev.u;
+  }
+  if (o.records) {
+    double *r = o.records + ((size_t)b * G1 + j) * kRecordWords;
+    r[kRecMt] = ev.mt;
+    r[kRecLst] = ev.lst;
+    r[kRecMd] = pair ? ev.md : 0.0;
+    r[kRecLsd] = pair ? ev.lsd : 0.0;
+    r[kRecLsz] = pair ? ev.lsz : 0.0;
+    r[kRecFlags] = (double)(ev.kind | (ev.err << 8) | (ev.key << 16));
+  }
+}
+
+__device__ __forceinline__ uint32_t flag_word(const DevParams &p, const PosEval &ev,
+                                              uint32_t outcome) {
+  return (p.epoch << 4) | (ev.near << 3) | (ev.key << 2) | outcome;
+}
+
+// The last item of sequence b to finish commits the round (verifier.cpp:223-256).
+__device__ void finalize_sequence(const DevOut &o, const DevScratch &s, const DevParams &p, int b) {
+  const int G1 = p.gamma + 1;
+  const unsigned int *fl = s.flags + (size_t)b * G1;
+  const int2 *slots = s.slots + (size_t)b * G1;
+  int keys = 0, nears = 0, k = p.gamma;
+  uint32_t outcome = kOutAccepted;
+  for (int j = 0; j < p.gamma; ++j) {
+    const uint32_t f = ld_acquire(fl + j);
+    keys += (f >> 2) & 1u;
+    nears += (f >> 3) & 1u;
+    outcome = f & 3u;
+    if (outcome != kOutAccepted) {
+      k = j;
+      break;
+    }
+  }
+  const int2 sl = slots[k];
+  o.accepted_count[b] = k;
+  o.key_count[b] = keys;
+  o.extra_source[b] = (k < p.gamma) ? DSDV_EXTRA_RESIDUAL : DSDV_EXTRA_BONUS;
+  o.extra_token[b] = sl.x;
+  o.status[b] = sl.y & 0xff;
+  o.near_threshold[b] = nears + ((sl.y >> 8) & 1);
+}
+
+__device__ __forceinline__ void complete_item(const DevOut &o, const DevScratch &s,
+                                              const DevParams &p, int b) {
+  __threadfence();
+  const unsigned prev = atomicAdd(s.done + b, 1u);
+  if (prev == (unsigned)p.gamma) {
+    __threadfence();
+    finalize_sequence(o, s, p, b);
+    s.done[b] = 0u;  // re-armed for the next window
+  }
+}
+
+// Resolve the element of tile `t` that holds T (warp-cooperative re-read).
+template <class In>
+__device__ __noinline__ int resolve_tile(const In *rt, const In *rd,
+                                            const Weigher<typename InTraits<In>::Acc> &wf, int t,
+                                            double run, double T, double W, double eps,
+                                            const DevParams &p, int lane, int &near,
+                                            bool want_last) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int VEC = InTraits<In>::kVec;
+  constexpr int CH = kRowBytes / (int)sizeof(In);
+  const int c = t / (kVecs * kCW), r = t - c * kVecs * kCW;
+  const int h = r / kCW, w = r - h * kCW;
+  const int id0 = c * CH + (h * kCT + w * 32 + lane) * VEC;
+  Acc vt[VEC], vd[VEC], wt[VEC];
+  const bool ok = id0 < p.vocab_local;
+  if (ok) {
+    unpack(ldg128(rt + id0), vt, (In *)nullptr);
+    if (wf.kind != kWeightPlain) {
+      unpack(ldg128(rd + id0), vd, (In *)nullptr);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) vd[e] = Acc(0);
+    }
+  }
+  double ls = 0.0;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    wt[e] = (ok && id0 + e < p.vocab_local) ? wf(vt[e], vd[e]) : Acc(0);
+    ls += (double)wt[e];
+  }
+  int result = -1;
+  if (want_last) {
+    // rounding-gap fallback: the last supported id of this tile
+    const unsigned sup = __ballot_sync(0xffffffffu, ls > 0.0);
+    const int src = sup ? 31 - __clz(sup) : -1;
+    int lastsup = -1;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+      if (wt[e] > Acc(0)) lastsup = id0 + e;
+    result = src >= 0 ? __shfl_sync(0xffffffffu, lastsup, src) : -1;
+    near = 1;
+    return result;
+  }
+  double incl = ls;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const double excl = run + (incl - ls);
+  const unsigned hit = __ballot_sync(0xffffffffu, ls > 0.0 && excl + ls > T);
+  int idx = -1, nr = 1;
+  if (hit) {
+    const int src = __ffs(hit) - 1;
+    if (lane == src) {
+      double cum = excl, margin = 0.0;
+      int lastsup = -1;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        if (idx < 0 && wt[e] > Acc(0)) {
+          lastsup = id0 + e;
+          const double nc = cum + (double)wt[e];
+          if (T < nc) {
+            idx = id0 + e;
+            margin = fmin(T - cum, nc - T);
+          }
+          cum = nc;
+        }
+      }
+      if (idx >= 0) {
+        nr = (margin < eps * W) ? 1 : 0;
+      } else {
+        idx = lastsup;
+        nr = 1;
+      }
+    }
+    idx = __shfl_sync(0xffffffffu, idx, src);
+    nr = __shfl_sync(0xffffffffu, nr, src);
+  } else {
+    // fp64 re-association gap between tile total and lane scan: upper edge
+    const unsigned sup = __ballot_sync(0xffffffffu, ls > 0.0);
+    const int src = sup ? 31 - __clz(sup) : -1;
+    int lastsup = -1;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+      if (wt[e] > Acc(0)) lastsup = id0 + e;
+    idx = src >= 0 ? __shfl_sync(0xffffffffu, lastsup, src) : -1;
+    nr = 1;
+  }
+  near = nr;
+  return idx;
+}
+
+template <class In>
+__device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
+                              const In *__restrict__ draft, const In *__restrict__ target,
+                              const int32_t *__restrict__ tokens, const DevOut &o,
+                              const DevScratch &s, int ew, int lane) {
+  using Acc = typename InTraits<In>::Acc;
+  const int G1 = p.gamma + 1;
+  const int M = p.top_m;
+  const double omt_d = (double)p.omt_f, tau_d = (double)p.tau_f;
+  const int nblocks = p.n_chunks * kVecs * kCW;
+  int *cand = sm.cand[ew];
+  for (int n = ew;; n += kEW) {
+    const int si = n % kSlots;
+    mbar_wait(&sm.part_full[si], (n / kSlots) & 1);
+    Slot<Acc> &sl = sm.slot[si];
+    const int item = sl.item;
+    if (item < 0) break;
+    const int j = item / p.B, b = item - j * p.B;
+    const bool pair = j < p.gamma;
+    const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
+    const In *rd = draft + ((size_t)b * p.gamma + (pair ? j : 0)) * (size_t)p.stride;
+    int2 *slotp = s.slots + (size_t)b * G1 + j;
+
+    if (sl.kind == kRegular) {
+      double mrg[5];
+      int diff = 0;
+      merge_partials(sl, p, lane, mrg, diff);
+      int shared = 0;
+      if (pair) {
+        const TopList<Acc> Lt = select_topm<In>(sl.u.bmax[0], nblocks, rt, M, p.vocab_local, cand, lane);
+        const TopList<Acc> Ld = select_topm<In>(sl.u.bmax[1], nblocks, rd, M, p.vocab_local, cand, lane);
+        bool found = false;
+        for (int k = 0; k < M; ++k) found |= (__shfl_sync(0xffffffffu, Lt.id, k) == Ld.id);
+        shared = __popc(__ballot_sync(0xffffffffu, found && lane < M));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.part_empty[si]);  // partials consumed
+
+      PosEval ev;
+      if (lane == 0) {
+        const int y = pair ? tokens[(size_t)b * p.gamma + j] : 0;
+        evaluate_position<In>(mrg, diff, shared, p, rt, rd, y, pair, ev);
+      }
+      const int need_exact = __shfl_sync(0xffffffffu, lane == 0 ? ev.need_exact : 0, 0);
+      if (need_exact) {
+        const double lse = exact_lse_mix_warp<In>(rt, rd, p.vocab_local, omt_d, tau_d, lane);
+        if (lane == 0) {
+          if (lse == -INFINITY)
+            ev.err = DSDV_E_DEGENERATE_MIXTURE;  // disjoint supports (verifier.cpp:181-184)
+          else
+            ev.lsz = lse - (omt_d * ev.mt + tau_d * ev.md);
+          ev.need_exact = 0;
+        }
+      }
+      if (lane == 0) {
+        if (pair) decide_position(p, b, j, ev);
+        write_position(o, p, b, j, pair, ev);
+        if (!p.stats_only) {
+          const unsigned int *fl = s.flags + (size_t)b * G1;
+          bool stopped_before = false;  // an earlier position already ends the window
+          if (!(pair && ev.accepted)) {
+            for (int jj = 0; jj < j && !stopped_before; ++jj) {
+              const uint32_t f = ld_acquire(fl + jj);
+              stopped_before = (f >> 4) == p.epoch && (f & 3u) != kOutAccepted;
+            }
+          }
+          int want = 0;  // 1 residual, 2 bonus
+          if (pair) {
+            if (!ev.accepted && !stopped_before) {
+              if (ev.err)
+                *slotp = make_int2(-1, ev.err);
+              else if (ev.kind == DSDV_EFF_DRAFT)
+                *slotp = make_int2(-1, DSDV_E_EMPTY_RESIDUAL);  // verifier.cpp:209-211
+              else
+                want = 1;
+            }
+          } else if (!stopped_before) {
+            if (ev.err)
+              *slotp = make_int2(-1, ev.err);
+            else
+              want = 2;
+          }
+          if (want) {
+            // the flag of a drawing position is published once its draw lands;
+            // stash it in the slot until then
+            if (pair) *slotp = make_int2(-2, (int)flag_word(p, ev, kOutRejected));
+            const int t = atomicAdd(&sm.req_tail, 1);
+            if (t - vload(&sm.req_done) >= kReq) __trap();  // queue bound
+            Request<Acc> &rq = sm.req[t % kReq];
+            rq.item = item;
+            rq.rows = want == 1 ? 2 : 1;
+            rq.u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b,
+                                       (uint32_t)(want == 1 ? p.gamma + j + 1 : 2 * p.gamma));
+            set_weigher(rq.wf,
+                        want == 2 ? kWeightPlain
+                                  : (ev.kind == DSDV_EFF_SOFTENED ? kWeightResSoft
+                                                                  : kWeightResTarget),
+                        ev, omt_d, tau_d);
+            __threadfence_block();
+            vstore(&rq.ready, 1);
+          } else {
+            if (pair) {
+              const uint32_t outcome =
+                  ev.err ? kOutError : (ev.accepted ? kOutAccepted : kOutRejected);
+              __threadfence();
+              st_release(s.flags + (size_t)b * G1 + j, flag_word(p, ev, outcome));
+            }
+            complete_item(o, s, p, b);
+          }
+        }
+      }
+    } else {
+      // ---- sample item: scan the tile sums for T = u W, resolve the tile ----
+      const Request<Acc> &rq = sm.req[sl.req];
+      const Weigher<Acc> wf = rq.wf;
+      const double u = rq.u;
+      const double *tiles = sl.u.tiles;
+      double wpart = 0.0;
+      for (int t = lane; t < nblocks; t += 32) wpart += tiles[t];
+      const double W = warp_sum_f64(wpart);
+      const double T = u * W;
+      double run = 0.0, base = 0.0;
+      int found = -1, lastpos = -1;
+      for (int c0 = 0; c0 < nblocks; c0 += 32) {
+        const int t = c0 + lane;
+        const double x = t < nblocks ? tiles[t] : 0.0;
+        const unsigned pos = __ballot_sync(0xffffffffu, x > 0.0);
+        if (pos) lastpos = c0 + 31 - __clz(pos);
+        if (found < 0) {
+          double incl = x;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, t < nblocks && x > 0.0 && run + incl > T);
+          if (hit) {
+            const int src = __ffs(hit) - 1;
+            found = c0 + src;
+            base = run + __shfl_sync(0xffffffffu, incl - x, src);
+          }
+          run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sm.part_empty[si]);  // tiles consumed
+        atomicAdd(&sm.req_done, 1);       // request entry free again
+      }
+      int near = 0, idx = -1;
+      if (W > 0.0) {
+        if (found >= 0)
+          idx = resolve_tile<In>(rt, rd, wf, found, base, T, W, p.eps_u, p, lane, near, false);
+        else
+          idx = resolve_tile<In>(rt, rd, wf, lastpos, 0.0, T, W, p.eps_u, p, lane, near, true);
+      }
+      if (lane == 0) {
+        if (pair) {
+          const int2 stash = *slotp;  // flag word stashed by the regular item
+          *slotp = idx < 0 ? make_int2(-1, DSDV_E_EMPTY_RESIDUAL)
+                           : make_int2(p.vocab_offset + idx, DSDV_OK | (near << 8));
+          __threadfence();
+          st_release(s.flags + (size_t)b * G1 + j, (uint32_t)stash.y);
+        } else {
+          *slotp = idx < 0 ? make_int2(-1, DSDV_E_EMPTY_RESIDUAL)
+                           : make_int2(p.vocab_offset + idx, DSDV_OK | (near << 8));
+        }
+        complete_item(o, s, p, b);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicAdd(&sm.epi_count, 1);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ producer warp
+template <class In>
+__device__ __forceinline__ void stream_rows(Smem<typename InTraits<In>::Acc> &sm, const In *rt,
+                                            const In *rd, bool two, int item, int kind, int n,
+                                            int req, int n_chunks, int nlocal, int &stage,
+                                            uint32_t &phase) {
+  constexpr int CH = kRowBytes / (int)sizeof(In);
+  for (int c = 0; c < n_chunks; ++c) {
+    mbar_wait(&sm.empty[stage], phase ^ 1);
+    StageMeta m;
+    m.item = item;
+    m.chunk = c;
+    m.kind = kind;
+    m.n = n;
+    m.req = req;
+    sm.meta[stage] = m;
+    const int rem = nlocal - c * CH;
+    const int elems = rem < CH ? rem : CH;
+    const uint32_t bytes = ((uint32_t)(elems * (int)sizeof(In)) + 15u) & ~15u;
+    mbar_arrive_expect_tx(&sm.full[stage], two ? 2u * bytes : bytes);
+    bulk_g2s(sm.ring[stage][1], rt + (size_t)c * CH, bytes, &sm.full[stage]);
+    if (two) bulk_g2s(sm.ring[stage][0], rd + (size_t)c * CH, bytes, &sm.full[stage]);
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+template <class In>
+__device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
+                              const In *__restrict__ draft, const In *__restrict__ target,
+                              const DevScratch &s) {
+  const int G1 = p.gamma + 1;
+  int stage = 0;
+  uint32_t phase = 0;
+  int n = 0;
+  bool exhausted = false;
+  for (;;) {
+    // sample requests first: their rows are still L2-resident
+    const int head = vload(&sm.req_head);
+    if (head != vload(&sm.req_tail)) {
+      const int r = head % kReq;
+      while (!vload(&sm.req[r].ready)) __nanosleep(32);  // entry still being written
+      __threadfence_block();
+      vstore(&sm.req[r].ready, 0);
+      const int item = sm.req[r].item;
+      const int two = sm.req[r].rows == 2;
+      const int j = item / p.B, b = item - j * p.B;
+      const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
+      const In *rd = draft + ((size_t)b * p.gamma + (j < p.gamma ? j : 0)) * (size_t)p.stride;
+      stream_rows<In>(sm, rt, rd, two, item, kSample, n, r, p.n_chunks, p.vocab_local, stage, phase);
+      ++n;
+      vstore(&sm.req_head, head + 1);
+      continue;
+    }
+    if (!exhausted) {
+      const int item = (int)atomicAdd(s.ticket, 1u);
+      if (item < p.n_items) {
+        const int j = item / p.B, b = item - j * p.B;  // position-major order
+        const bool pair = j < p.gamma;
+        const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
+        const In *rd = draft + ((size_t)b * p.gamma + (pair ? j : 0)) * (size_t)p.stride;
+        stream_rows<In>(sm, rt, rd, pair, item, kRegular, n, 0, p.n_chunks, p.vocab_local, stage,
+                        phase);
+        ++n;
+        continue;
+      }
+      exhausted = true;
+    }
+    // drained: wait until the epilogue has seen everything streamed, then
+    // re-check for requests it may have posted on the way
+    if (vload(&sm.epi_count) == n) {
+      __threadfence_block();
+      if (vload(&sm.req_head) == vload(&sm.req_tail)) break;
+      continue;
+    }
+    __nanosleep(256);
+  }
+  // end of stream
+  mbar_wait(&sm.empty[stage], phase ^ 1);
+  StageMeta m;
+  m.item = -1;
+  m.chunk = 0;
+  m.kind = kRegular;
+  m.n = n;
+  m.req = 0;
+  sm.meta[stage] = m;
+  mbar_arrive(&sm.full[stage]);
+}
+
+// ------------------------------------------------------------------ kernel
+template <class In>
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_verify_kernel(const __grid_constant__ DevParams p, const In *__restrict__ draft,
+                        const In *__restrict__ target, const int32_t *__restrict__ tokens,
+                        const __grid_constant__ DevOut o, const __grid_constant__ DevScratch s) {
+  using Acc = typename InTraits<In>::Acc;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem<Acc> &sm = *reinterpret_cast<Smem<Acc> *>(smem_raw);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], kCW);
+    }
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&sm.part_full[i], kCW);
+      mbar_init(&sm.part_empty[i], 1);
+    }
+    sm.req_head = sm.req_tail = sm.req_done = 0;
+    sm.epi_count = sm.epi_exit = 0;
+    for (int i = 0; i < kReq; ++i) sm.req[i].ready = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kProdWarp) {
+    if (lane == 0) producer_loop<In>(sm, p, draft, target, s);
+  } else if (warp >= kEpiWarp) {
+    epilogue_loop<In>(sm, p, draft, target, tokens, o, s, warp - kEpiWarp, lane);
+    if (lane == 0 && atomicAdd(&sm.epi_exit, 1) == kEW - 1) {
+      // last CTA out re-arms the work counters for the next launch
+      __threadfence();
+      const unsigned prev = atomicAdd(s.exit_count, 1u);
+      if (prev == gridDim.x - 1) {
+        *s.ticket = 0u;
+        *s.exit_count = 0u;
+        __threadfence();
+      }
+    }
+  } else {
+    if (p.need_z)
+      compute_loop<In, true>(sm, p, tid);
+    else
+      compute_loop<In, false>(sm, p, tid);
+  }
+}
+
+}  // namespace fz
+
+// ------------------------------------------------------------------ launch
+template <class In>
+cudaError_t launch_fused(const DevParams &p, const void *draft, const void *target,
+                         const int32_t *tokens, const DevOut &o, const DevScratch &s,
+                         cudaStream_t stream, int *grid_out) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int CH = fz::kRowBytes / (int)sizeof(In);
+  DevParams q = p;
+  q.n_chunks = (p.vocab_local + CH - 1) / CH;
+  if (q.n_chunks * fz::kVecs * fz::kCW > fz::kMaxTiles) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(fz::Smem<Acc>);
+  // occupancy is a property of (kernel, device): query once per device
+  static int cached_device = -1, cached_grid_cap = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (cached_device != dev) {
+    e = cudaFuncSetAttribute(fz::fused_verify_kernel<In>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fz::fused_verify_kernel<In>,
+                                                      fz::kThreads, smem);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    cached_grid_cap = per_sm * sms;
+    cached_device = dev;
+  }
+  int grid = cached_grid_cap;
+  if (grid > q.n_items) grid = q.n_items;
+  if (grid_out) *grid_out = grid;
+  fz::fused_verify_kernel<In><<<grid, fz::kThreads, smem, stream>>>(
+      q, (const In *)draft, (const In *)target, tokens, o, s);
+  return cudaGetLastError();
+}
+
+// Vocabulary limit of the fused kernel for a dtype (sample tiles per slot).
+int fused_max_vocab(int esize) {
+  return fz::kMaxTiles / (fz::kVecs * fz::kCW) * (fz::kRowBytes / esize);
+}
+
+template cudaError_t launch_fused<__nv_bfloat16>(const DevParams &, const void *, const void *,
+                                                 const int32_t *, const DevOut &,
+                                                 const DevScratch &, cudaStream_t, int *);
+template cudaError_t launch_fused<float>(const DevParams &, const void *, const void *,
+                                         const int32_t *, const DevOut &, const DevScratch &,
+                                         cudaStream_t, int *);
+template cudaError_t launch_fused<double>(const DevParams &, const void *, const void *,
+                                          const int32_t *, const DevOut &, const DevScratch &,
+                                          cudaStream_t, int *);
+
+}  // namespace dsdv

@@ -1,0 +1,123 @@
+"""Parity of the fused sm_100a verifier (dsdv_verify) with the fp64 oracle.
+
+Runs through the C-ABI on the GPU. Inputs are the seeded synthetic row
+families of SURVEY.md §8(d) (Zipf and Gaussian, b mod 4), generated on the
+device and copied back; draft tokens are drawn by the oracle with the Philox
+draft slots, exactly as verify_round's draft_window would (verifier.cpp:93-110).
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.parity_util import compare_window, run_gpu_window
+
+pytestmark = pytest.mark.gpu
+
+
+def _crit(oracle, r=2.0, g=0.2, o=0.5, m=10):
+    return oracle.crit(r, g, o, m)
+
+
+def _check(rep, max_eps_frac=0.05):
+    assert rep.ok(), rep.mismatches[:10]
+    assert rep.eps_events <= max(1, int(max_eps_frac * rep.sequences)), rep.eps_events
+
+
+def test_c1_shape_fp32(verifier, oracle):
+    """C1: V=32000, gamma=4, tau=0.2, fp32 (batch 16 instead of 1 for coverage)."""
+    d, t, tok, gpu, _ = run_gpu_window(verifier, torch.float32, 16, 4, 32000, 0.2,
+                                       _crit(oracle), seed=1, oracle=oracle)
+    rep = compare_window(oracle, d, t, tok, gpu, 0.2, _crit(oracle), seed=1, window=0)
+    _check(rep)
+    assert rep.positions_checked == 16 * 4
+
+
+def test_c2_vocab_bf16(verifier, oracle):
+    """C2 shape per sequence: V=128256, gamma=8, bf16 logits."""
+    d, t, tok, gpu, _ = run_gpu_window(verifier, torch.bfloat16, 8, 8, 128256, 0.2,
+                                       _crit(oracle), seed=2, oracle=oracle)
+    rep = compare_window(oracle, d, t, tok, gpu, 0.2, _crit(oracle), seed=2, window=0)
+    _check(rep)
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.5, 1.0])
+def test_tau_endpoints_and_mid(verifier, oracle, tau):
+    d, t, tok, gpu, _ = run_gpu_window(verifier, torch.float32, 12, 6, 5000, tau,
+                                       _crit(oracle), seed=3, oracle=oracle)
+    rep = compare_window(oracle, d, t, tok, gpu, tau, _crit(oracle), seed=3, window=0)
+    _check(rep)
+
+
+@pytest.mark.parametrize("V", [2, 7, 1000, 4099])
+def test_ragged_vocab(verifier, oracle, V):
+    """Vocabularies that are not a multiple of the vector / chunk width."""
+    m = min(10, V)
+    d, t, tok, gpu, _ = run_gpu_window(verifier, torch.float32, 8, 3, V, 0.3,
+                                       _crit(oracle, m=m), seed=4, oracle=oracle)
+    rep = compare_window(oracle, d, t, tok, gpu, 0.3, _crit(oracle, m=m), seed=4, window=0)
+    _check(rep)
+
+
+def test_all_key_thresholds(verifier, oracle):
+    """gap_limit 0 and ratio 1e-9 mark everything key (acceptance.cpp:204)."""
+    c = _crit(oracle, r=1e-9, g=0.0, o=1.0, m=1)
+    d, t, tok, gpu, _ = run_gpu_window(verifier, torch.float32, 8, 4, 3000, 0.9, c, seed=5,
+                                       oracle=oracle)
+    rep = compare_window(oracle, d, t, tok, gpu, 0.9, c, seed=5, window=0)
+    _check(rep)
+    assert gpu["key_mask"].all()
+
+
+def test_no_key_tau_one_accepts_everything(verifier, oracle):
+    """KeyCriteria::none() + tau=1: every window is accepted (test_verifier.cpp:245-254)."""
+    c = _crit(oracle, r=float("inf"), g=1.0, o=0.0, m=1)
+    d, t, tok, gpu, _ = run_gpu_window(verifier, torch.float32, 16, 4, 2000, 1.0, c, seed=6,
+                                       oracle=oracle)
+    assert (gpu["accepted_count"] == 4).all()
+    assert (gpu["extra_source"] == 0).all()
+    assert not gpu["key_mask"].any()
+
+
+def test_identical_rows_accept_whole_window(verifier, oracle):
+    """Identical draft/target rows: a == 1 everywhere (test_verifier.cpp:233-243)."""
+    from paper_2511_11733_b200.dsdv import VerifyParams
+    B, G, V = 8, 5, 3001
+    draft, target = verifier.synth_logits(B, G, V, torch.float32, logits_seed=9)
+    target[:, :G].copy_(draft)
+    tokens = torch.randint(0, V, (B, G), dtype=torch.int32, device=draft.device)
+    p = VerifyParams(gamma=G, tau=0.0, ratio_limit=float("inf"), gap_limit=1.0,
+                     overlap_floor=0.0, top_m=1, seed=7)
+    out = verifier.verify(draft, target, tokens, p, vocab=V)
+    verifier.sync(p, out, batch=B, vocab=V)
+    h = out.to_host()
+    assert (h["accepted_count"] == G).all()
+    assert (h["accept_prob"] == 1.0).all()
+
+
+def test_windows_are_independent_of_launch_history(verifier, oracle):
+    """Same inputs, same seed/window -> bit-identical results across launches
+    (test_verifier.cpp:306-324); a different window index changes the draws."""
+    d, t, tok, gpu1, (draft, target, tokens, p) = run_gpu_window(
+        verifier, torch.bfloat16, 16, 8, 20000, 0.2, _crit(oracle), seed=11, oracle=oracle)
+    outs = []
+    for _ in range(3):
+        o = verifier.verify(draft, target, tokens, p, vocab=20000)
+        verifier.sync(p, o, batch=16, vocab=20000)
+        outs.append(o.to_host())
+    for o in outs:
+        for k in ("accepted_count", "extra_token", "extra_source", "key_mask", "accept_prob"):
+            assert torch.equal(o[k], gpu1[k]), k
+
+
+def test_draft_sample_matches_oracle(verifier, oracle):
+    """Draft-side step (draft_window, verifier.cpp:93-110) on the device."""
+    from paper_2511_11733_b200.dsdv import VerifyParams
+    from tests.parity_util import host_rows, oracle_draft_tokens
+    B, G, V = 16, 4, 32000
+    draft, _ = verifier.synth_logits(B, G, V, torch.float32, logits_seed=13)
+    p = VerifyParams(gamma=G, seed=21, window=3)
+    tok = verifier.draft_sample(draft, p, vocab=V)
+    torch.cuda.synchronize()
+    ref = oracle_draft_tokens(oracle, host_rows(draft, V), 21, 3)
+    mism = (tok.cpu().numpy() != ref).sum()
+    assert mism <= 1, mism
