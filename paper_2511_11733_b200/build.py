@@ -51,24 +51,29 @@ def _headers() -> list[Path]:
     return sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.rglob("*.h")) + sorted(INCLUDE.rglob("*.hpp"))
 
 
-def build_dsdv(force: bool = False) -> Path:
+def build_dsdv(force: bool = False, trace: bool = False) -> Path:
+    """libdsdv.so; trace=True builds the cycle-accounting variant
+    libdsdv_trace.so (-DDSDV_TRACE, development aid, load with DSDV_LIB)."""
     hdrs = _headers()
-    if not force and not _stale(LIB_DSDV, [*(CSRC / s for s in CU_SOURCES), *hdrs]):
-        return LIB_DSDV  # up to date (also on GPU boxes, where build/ is not shipped)
-    BUILD.mkdir(exist_ok=True)
+    lib = PKG / "libdsdv_trace.so" if trace else LIB_DSDV
+    bdir = BUILD / ("trace" if trace else "release")
+    flags = [*NVCC_FLAGS, *(["-DDSDV_TRACE"] if trace else [])]
+    if not force and not _stale(lib, [*(CSRC / s for s in CU_SOURCES), *hdrs]):
+        return lib  # up to date (also on GPU boxes, where build/ is not shipped)
+    bdir.mkdir(parents=True, exist_ok=True)
     objs = []
     jobs = []
     for src in CU_SOURCES:
         s = CSRC / src
-        o = BUILD / (s.stem + ".o")
+        o = bdir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s, *hdrs]):
-            jobs.append([NVCC, *NVCC_FLAGS, "-c", str(s), "-o", str(o)])
+            jobs.append([NVCC, *flags, "-c", str(s), "-o", str(o)])
     with ThreadPoolExecutor(max_workers=min(4, max(1, len(jobs)))) as ex:
         list(ex.map(_run, jobs))
-    if force or jobs or _stale(LIB_DSDV, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", str(LIB_DSDV), *map(str, objs)])
-    return LIB_DSDV
+    if force or jobs or _stale(lib, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", str(lib), *map(str, objs)])
+    return lib
 
 
 def build_dsd_api(force: bool = False) -> Path | None:
@@ -89,5 +94,8 @@ def build_all(force: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    build_all(force="--force" in sys.argv)
-    print(LIB_DSDV)
+    if "--trace" in sys.argv:
+        print(build_dsdv(force="--force" in sys.argv, trace=True))
+    else:
+        build_all(force="--force" in sys.argv)
+        print(LIB_DSDV)

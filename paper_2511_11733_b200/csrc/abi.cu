@@ -12,7 +12,7 @@
 #include "common.cuh"
 
 namespace dsdv {
-int fused_max_vocab(int esize);
+int fused_max_vocab(int esize, int top_m);
 template <class In>
 cudaError_t launch_fused(const DevParams &, const void *, const void *, const int32_t *,
                          const DevOut &, const DevScratch &, cudaStream_t, int *);
@@ -33,6 +33,7 @@ struct dsdv_ctx {
   unsigned int *flags = nullptr;  // [positions]
   int2 *slots = nullptr;          // [positions]
   unsigned int *done = nullptr;   // [sequences]
+  unsigned long long *trace = nullptr;  // DSDV_TRACE builds: [grid][kTraceWords]
   size_t flags_cap = 0;
   size_t done_cap = 0;
   uint32_t epoch = 0;
@@ -96,6 +97,7 @@ dsdv_status ensure_scratch(dsdv_ctx *ctx, size_t n_positions, size_t n_sequences
   }
   if (n_sequences > ctx->done_cap) {
     if (ctx->done) cudaFree(ctx->done);
+  if (ctx->trace) cudaFree(ctx->trace);
     e = cudaMalloc(&ctx->done, n_sequences * sizeof(unsigned int));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(done)");
     e = cudaMemset(ctx->done, 0, n_sequences * sizeof(unsigned int));
@@ -197,6 +199,14 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   s.flags = ctx->flags;
   s.slots = ctx->slots;
   s.done = ctx->done;
+  s.trace = nullptr;
+#ifdef DSDV_TRACE
+  if (!ctx->trace) {
+    cudaMalloc(&ctx->trace, 1024 * dsdv::kTraceWords * sizeof(unsigned long long));
+    cudaMemset(ctx->trace, 0, 1024 * dsdv::kTraceWords * sizeof(unsigned long long));
+  }
+  s.trace = ctx->trace;
+#endif
   const DevOut o = to_dev(out);
   switch (params->dtype) {
     case DSDV_DTYPE_BF16:
@@ -251,6 +261,7 @@ dsdv_status dsdv_destroy(dsdv_ctx *ctx) {
   if (ctx->flags) cudaFree(ctx->flags);
   if (ctx->slots) cudaFree(ctx->slots);
   if (ctx->done) cudaFree(ctx->done);
+  if (ctx->trace) cudaFree(ctx->trace);
   delete ctx;
   return DSDV_OK;
 }
@@ -260,6 +271,23 @@ const char *dsdv_last_error(const dsdv_ctx *ctx) {
 }
 
 uint64_t dsdv_launch_count(const dsdv_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+// Development aid (not part of the ABI header): copies and clears the per-CTA
+// cycle counters of a DSDV_TRACE build. Returns the number of CTAs, 0 if the
+// library was built without tracing.
+int dsdv_debug_trace(dsdv_ctx *ctx, unsigned long long *host, int max_ctas) {
+#ifdef DSDV_TRACE
+  if (!ctx || !ctx->trace) return 0;
+  const int n = max_ctas < 1024 ? max_ctas : 1024;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, ctx->trace, (size_t)n * dsdv::kTraceWords * 8, cudaMemcpyDeviceToHost);
+  cudaMemset(ctx->trace, 0, 1024 * dsdv::kTraceWords * 8);
+  return ctx->last_grid;
+#else
+  (void)ctx; (void)host; (void)max_ctas;
+  return 0;
+#endif
+}
 
 double dsdv_uniform(uint64_t seed, uint64_t window, uint32_t sequence, uint32_t slot) {
   return dsdv_philox_uniform(seed, window, sequence, slot);
@@ -300,10 +328,11 @@ dsdv_status dsdv_validate(dsdv_ctx *ctx, const dsdv_params *pp) {
     return fail(ctx, DSDV_E_UNSUPPORTED,
                 "row_stride %d must be >= %d and a multiple of %d elements (16-byte rows)",
                 p.row_stride, need, vec);
-  if (p.vocab_local > dsdv::fused_max_vocab(es))
-    return fail(ctx, DSDV_E_UNSUPPORTED, "vocab slice %d exceeds the fused kernel limit %d for this dtype",
-                p.vocab_local, dsdv::fused_max_vocab(es));
   const int m = p.top_m < p.vocab ? p.top_m : p.vocab;
+  if (p.vocab_local > dsdv::fused_max_vocab(es, m))
+    return fail(ctx, DSDV_E_UNSUPPORTED,
+                "vocab slice %d exceeds the fused kernel limit %d for this dtype and top_m",
+                p.vocab_local, dsdv::fused_max_vocab(es, m));
   if (m > dsdv::kMaxTopM)
     return fail(ctx, DSDV_E_UNSUPPORTED, "top_m %d exceeds the kernel limit %d", m,
                 dsdv::kMaxTopM);

@@ -65,7 +65,9 @@ struct DevScratch {
   unsigned int *flags;       // [B][gamma+1] per-position outcome words (epoch-tagged)
   int2 *slots;               // [B][gamma+1] extra-token draws (token, status | near << 8)
   unsigned int *done;        // [B] items finished this window (reset by the finaliser)
+  unsigned long long *trace; // [grid][kTraceWords] cycle counters (DSDV_TRACE builds only)
 };
+constexpr int kTraceWords = 24;
 
 // ------------------------------------------------------------------ traits
 template <class In>
@@ -140,16 +142,8 @@ __device__ __forceinline__ f32x2 pk2(float lo, float hi) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
   return r;
 }
-__device__ __forceinline__ float lo2(f32x2 a) {
-  float l, h;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(a));
-  return l;
-}
-__device__ __forceinline__ float hi2(f32x2 a) {
-  float l, h;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(a));
-  return h;
-}
+__device__ __forceinline__ float lo2(f32x2 a) { return __uint_as_float((unsigned)a); }
+__device__ __forceinline__ float hi2(f32x2 a) { return __uint_as_float((unsigned)(a >> 32)); }
 __device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
   f32x2 r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));

@@ -38,6 +38,8 @@
 // rejection (:223-250), k, extra token, key count.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "common.cuh"
 #include "sample.cuh"
 
@@ -52,14 +54,43 @@ constexpr int kProdWarp = kCW + kEW; // producer warp index
 constexpr int kThreads = (kCW + kEW + 1) * 32;
 constexpr int kRowBytes = 16384;     // per row per ring stage
 constexpr int kVecs = kRowBytes / 16 / kCT;  // 16-byte vectors per compute thread per row (4)
-constexpr int kStages = 4;
 constexpr int kSlots = 4;
+// ring depth: 4 x 32 KB stages (3 for fp64 rows, whose slots are larger)
+template <class Acc>
+struct Ring {
+  static constexpr int kStages = sizeof(Acc) == 8 ? 3 : 4;
+};
 constexpr int kMaxTiles = 2048;      // blocks per slot: (chunk, vector, warp), 32*VEC ids each
+constexpr int kAreaBytes = 20480;    // per-slot block maxima + published lists, or sample tiles
 constexpr int kReq = 16;             // sample-request queue
 constexpr float kSlack = 8.0f;       // lazy max: rescale when a value exceeds m by this much
 constexpr float kFloorM = -1e30f;    // finite "empty" max (keeps (v - m) free of inf - inf)
 
 enum ItemKind : int { kRegular = 0, kSample = 1 };
+
+// Optional cycle accounting per CTA (compile with -DDSDV_TRACE; see
+// scripts/trace_roles.py): where each warp role spends its time.
+enum TraceWord : int {
+  kTrComputeWaitFull = 0, kTrComputeFold, kTrComputeSample, kTrComputeWaitSlot, kTrComputeItemEnd,
+  kTrEpiWaitFull, kTrEpiMerge, kTrEpiTopm, kTrEpiDecide, kTrEpiSample, kTrProdWaitEmpty,
+  kTrProdDrain, kTrProdItems, kTrProdSamples, kTrKernel, kTrEpiItems, kTrTopmCand, kTrTopmIns,
+  kTrTopmFallback, kTrMaxSurv, kTrNeedExact
+};
+#ifdef DSDV_TRACE
+#define TR_START(v) const long long v = clock64()
+#define TR_ADD(tr, w, v)                                                         \
+  do {                                                                           \
+    if (tr) atomicAdd((tr) + (w), (unsigned long long)(clock64() - (v)));       \
+  } while (0)
+#define TR_INC(tr, w)             \
+  do {                            \
+    if (tr) atomicAdd((tr) + (w), 1ull); \
+  } while (0)
+#else
+#define TR_START(v) (void)0
+#define TR_ADD(tr, w, v) (void)0
+#define TR_INC(tr, w) (void)0
+#endif
 
 struct StageMeta {
   int item;   // global item id (b, j), -1 = end of stream
@@ -73,6 +104,7 @@ template <class Acc>
 struct WarpPartial {
   Acc mt, st, md, sd, sz;
   int diff;
+  int kt[2], kd[2];  // the warp's two largest block keys of each row
 };
 
 template <class Acc>
@@ -81,10 +113,28 @@ struct Slot {
   int kind;
   int req;
   WarpPartial<Acc> wp[kCW];
-  union {
-    int bmax[2][kMaxTiles];  // regular item: per-block max keys of l_t / l_d (top-m candidates)
-    double tiles[kMaxTiles];  // sample item: per-block weight sums
-  } u;
+  // regular item: per-block max keys of l_t / l_d ([2][nblocks] ints), then each
+  // warp's M largest block keys and block indices ([2][kCW][M] ints, twice);
+  // sample item: per-block weight sums ([nblocks] doubles). See SlotView.
+  alignas(16) uint8_t area[kAreaBytes];
+};
+
+// Typed views of a slot's area for one launch shape.
+struct SlotView {
+  int *bmax[2];
+  int *pkey[2];  // [kCW][M]
+  int *pblk[2];  // [kCW][M]
+  double *tiles;
+  __device__ __forceinline__ SlotView(uint8_t *area, int nblocks, int M) {
+    int *a = reinterpret_cast<int *>(area);
+    bmax[0] = a;
+    bmax[1] = a + nblocks;
+    pkey[0] = a + 2 * nblocks;
+    pkey[1] = pkey[0] + kCW * M;
+    pblk[0] = pkey[1] + kCW * M;
+    pblk[1] = pblk[0] + kCW * M;
+    tiles = reinterpret_cast<double *>(area);
+  }
 };
 
 template <class Acc>
@@ -96,8 +146,16 @@ struct Request {
   Weigher<Acc> wf;
 };
 
+struct EpiScratch {
+  int cand[32];          // candidate blocks of one 32-block batch
+  int ev_id[128];        // surviving elements (id, value)
+  double ev_key[128];
+  int sel[2][kMaxTopM];  // top-m ids of the target / draft row
+};
+
 template <class Acc>
 struct alignas(128) Smem {
+  static constexpr int kStages = Ring<Acc>::kStages;
   uint8_t ring[kStages][2][kRowBytes];  // [stage][0 = draft, 1 = target]
   Slot<Acc> slot[kSlots];
   Request<Acc> req[kReq];
@@ -109,7 +167,7 @@ struct alignas(128) Smem {
   int req_done;            // sample items finished (entries free again)
   int epi_count;           // stream items the epilogue warps have finished
   int epi_exit;            // epilogue warps that have left
-  int cand[kEW][32];       // epilogue scratch: candidate blocks of a batch
+  EpiScratch epi[kEW];     // per epilogue warp: top-m selection scratch
 };
 
 // ------------------------------------------------------------------ helpers
@@ -141,12 +199,19 @@ template <class Acc>
 struct ItemState {
   Acc mt, st, md, sd, sz;
   uint32_t diff;
+  int kt1, kt2, kd1, kd2;  // warp's two largest block keys per row (warp-uniform)
   __device__ __forceinline__ void reset() {
     mt = md = Acc(kFloorM);
     st = sd = sz = Acc(0);
     diff = 0;
+    kt1 = kt2 = kd1 = kd2 = INT_MIN;
   }
 };
+
+__device__ __forceinline__ void top2_key(int &k1, int &k2, int key) {
+  k2 = key > k1 ? k1 : (key > k2 ? key : k2);
+  k1 = key > k1 ? key : k1;
+}
 
 __device__ __forceinline__ int warp_max_key(int key) {
   int r;
@@ -256,6 +321,8 @@ __device__ __forceinline__ void fold_vec(const uint8_t *sdraft, const uint8_t *s
     for (int e = 1; e < VEC; ++e) cmd = vmax(cmd, vd[e]);
     const int bt = warp_max_key(fkey(cmt));
     const int bd = warp_max_key(fkey(cmd));
+    top2_key(S.kt1, S.kt2, bt);
+    top2_key(S.kd1, S.kd2, bd);
     if (lane == 0) {
       bmax_t[bi] = bt;
       bmax_d[bi] = bd;
@@ -310,8 +377,51 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
   }
 }
 
+// Item end, per compute warp and row: publish this warp's M largest block
+// keys (and block indices) by M warp-uniform max extractions. The global top-M
+// blocks lie in the union of these lists, so the epilogue never scans all
+// blocks.
+__device__ __forceinline__ void publish_top_blocks(const SlotView &sv, int r, const DevParams &p,
+                                                   int warp, int lane) {
+  const int M = p.top_m;
+  const int nbw = p.n_chunks * kVecs;  // this warp's blocks: i -> (chunk i / kVecs, vector i % kVecs)
+  constexpr int kPer = kMaxTiles / kCW / 32;  // keys per lane (<= 4)
+  int key[kPer];
+#pragma unroll
+  for (int t = 0; t < kPer; ++t) {
+    const int i = t * 32 + lane;
+    key[t] = i < nbw ? sv.bmax[r][((i / kVecs) * kVecs + (i % kVecs)) * kCW + warp] : INT_MIN;
+  }
+  for (int m = 0; m < M; ++m) {
+    int lm = INT_MIN, lt = 0;
+#pragma unroll
+    for (int t = 0; t < kPer; ++t)
+      if (key[t] > lm) {
+        lm = key[t];
+        lt = t;
+      }
+    const int gm = warp_max_key(lm);
+    // lowest lane holding the maximum gives it up (ties leave one at a time)
+    const unsigned own = __ballot_sync(0xffffffffu, lm == gm);
+    const int src = __ffs(own) - 1;
+    const int bi_local = __shfl_sync(0xffffffffu, lt * 32 + lane, src);
+    if (lane == src) {
+#pragma unroll
+      for (int t = 0; t < kPer; ++t)
+        if (t == lt) key[t] = INT_MIN;
+    }
+    if (lane == 0) {
+      sv.pkey[r][warp * M + m] = gm;
+      sv.pblk[r][warp * M + m] =
+          bi_local < nbw ? ((bi_local / kVecs) * kVecs + (bi_local % kVecs)) * kCW + warp : -1;
+    }
+  }
+}
+
 template <class In, bool NEEDZ>
-__device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p, int tid) {
+__device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
+                             const In *__restrict__ draft, const In *__restrict__ target, int tid,
+                             unsigned long long *tr) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
@@ -322,8 +432,11 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
   uint32_t phase = 0;
   bool pair = false;
   int kind = kRegular, n = 0, s = 0;
+  unsigned long long *trl = (tid & 31) == 0 ? tr : nullptr;
   for (;;) {
+    TR_START(tw);
     mbar_wait(&sm.full[stage], phase);
+    TR_ADD(trl, kTrComputeWaitFull, tw);
     const StageMeta md = sm.meta[stage];
     if (md.item < 0) {
       // end of stream: one terminating slot per epilogue warp
@@ -343,14 +456,18 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       s = n % kSlots;
       const int j = md.item / p.B;
       pair = j < p.gamma;
-      // the slot (partials + thresholds) must be free before this item runs
+      // the slot (partials + block maxima) must be free before this item runs
+      TR_START(ts);
       mbar_wait(&sm.part_empty[s], ((n / kSlots) & 1) ^ 1);
+      TR_ADD(trl, kTrComputeWaitSlot, ts);
     }
     const bool last = c == p.n_chunks - 1;
+    TR_START(tf);
     if (kind == kRegular) {
       const bool tail = last && (p.vocab_local % CH) != 0;
-      int *bt = sm.slot[s].u.bmax[0];
-      int *bd = sm.slot[s].u.bmax[1];
+      const SlotView sv(sm.slot[s].area, p.n_chunks * kVecs * kCW, p.top_m);
+      int *bt = sv.bmax[0];
+      int *bd = sv.bmax[1];
       if (pair) {
 #pragma unroll 1
         for (int h = 0; h < kVecs; ++h) {
@@ -368,17 +485,19 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       }
     } else {
       sample_chunk<In>(sm.ring[stage][0], sm.ring[stage][1], c, sm.req[md.req].wf,
-                       sm.slot[s].u.tiles, p, tid, warp, lane);
+                       reinterpret_cast<double *>(sm.slot[s].area), p, tid, warp, lane);
     }
+    TR_ADD(trl, kind == kRegular ? kTrComputeFold : kTrComputeSample, tf);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[stage]);
-    if (++stage == kStages) {
+    if (++stage == Smem<Acc>::kStages) {
       stage = 0;
       phase ^= 1;
     }
     if (!last) continue;
 
     // ---- item end: publish this warp's partial, never wait for the epilogue ----
+    TR_START(te);
     Slot<Acc> &sl = sm.slot[s];
     if (kind == kRegular) {
       const Acc omt = Acc(p.omt_f), tau = Acc(p.tau_f), L = log2e<Acc>();
@@ -406,9 +525,18 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
         w.sd = S.sd;
         w.sz = S.sz;
         w.diff = anydiff;
+        w.kt[0] = S.kt1;
+        w.kt[1] = S.kt2;
+        w.kd[0] = S.kd1;
+        w.kd[1] = S.kd2;
         sl.wp[warp] = w;
       }
       S.reset();
+      if (pair) {
+        const SlotView sv(sl.area, p.n_chunks * kVecs * kCW, p.top_m);
+        publish_top_blocks(sv, 0, p, warp, lane);
+        publish_top_blocks(sv, 1, p, warp, lane);
+      }
     }
     if (tid == 0) {
       sl.item = md.item;
@@ -417,165 +545,171 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.part_full[s]);
+    TR_ADD(trl, kTrComputeItemEnd, te);
   }
 }
 
 // ------------------------------------------------------------------ epilogue warp
-// fp64 merge of the kCW warp partials (lanes 0..kCW-1, xor tree).
+// Merge of the kCW warp partials (lanes 0..kCW-1, xor tree) in the
+// accumulation precision, widened to fp64 at the end.
 template <class Acc>
 __device__ __noinline__ void merge_partials(const Slot<Acc> &sl, const DevParams &p, int lane,
-                                               double (&out)[5], int &diff) {
-  double mt = -INFINITY, st = 0.0, md = -INFINITY, sd = 0.0, sz = 0.0;
+                                            double (&out)[5], int &diff) {
+  const Acc L = log2e<Acc>();
+  Acc mt = Acc(kFloorM), st = Acc(0), md = Acc(kFloorM), sd = Acc(0), sz = Acc(0);
   int df = 0;
   if (lane < kCW) {
     const WarpPartial<Acc> w = sl.wp[lane];
-    mt = (double)w.mt;
-    st = (double)w.st;
-    md = (double)w.md;
-    sd = (double)w.sd;
-    sz = (double)w.sz;
+    mt = w.mt;
+    st = w.st;
+    md = w.md;
+    sd = w.sd;
+    sz = w.sz;
     df = w.diff;
   }
-  const double omt = (double)p.omt_f, tau = (double)p.tau_f;
-#pragma unroll 1
+  const Acc omt = Acc(p.omt_f), tau = Acc(p.tau_f);
+#pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    const double mt2 = __shfl_xor_sync(0xffffffffu, mt, off);
-    const double st2 = __shfl_xor_sync(0xffffffffu, st, off);
-    const double md2 = __shfl_xor_sync(0xffffffffu, md, off);
-    const double sd2 = __shfl_xor_sync(0xffffffffu, sd, off);
-    const double sz2 = __shfl_xor_sync(0xffffffffu, sz, off);
+    const Acc mt2 = __shfl_xor_sync(0xffffffffu, mt, off);
+    const Acc st2 = __shfl_xor_sync(0xffffffffu, st, off);
+    const Acc md2 = __shfl_xor_sync(0xffffffffu, md, off);
+    const Acc sd2 = __shfl_xor_sync(0xffffffffu, sd, off);
+    const Acc sz2 = __shfl_xor_sync(0xffffffffu, sz, off);
     df |= __shfl_xor_sync(0xffffffffu, df, off);
-    const double Mn = fmax(mt, mt2), Dn = fmax(md, md2);
-    sz = (sz != 0.0 ? sz * exp(omt * (mt - Mn) + tau * (md - Dn)) : 0.0) +
-         (sz2 != 0.0 ? sz2 * exp(omt * (mt2 - Mn) + tau * (md2 - Dn)) : 0.0);
-    st = (st != 0.0 ? st * exp(mt - Mn) : 0.0) + (st2 != 0.0 ? st2 * exp(mt2 - Mn) : 0.0);
-    sd = (sd != 0.0 ? sd * exp(md - Dn) : 0.0) + (sd2 != 0.0 ? sd2 * exp(md2 - Dn) : 0.0);
+    const Acc Mn = vmax(mt, mt2), Dn = vmax(md, md2);
+    st = st * fast_exp2((mt - Mn) * L) + st2 * fast_exp2((mt2 - Mn) * L);
+    sd = sd * fast_exp2((md - Dn) * L) + sd2 * fast_exp2((md2 - Dn) * L);
+    sz = sz * fast_exp2((omt * (mt - Mn) + tau * (md - Dn)) * L) +
+         sz2 * fast_exp2((omt * (mt2 - Mn) + tau * (md2 - Dn)) * L);
     mt = Mn;
     md = Dn;
   }
-  out[0] = mt;
-  out[1] = st;
-  out[2] = md;
-  out[3] = sd;
-  out[4] = sz;
+  out[0] = (double)mt;
+  out[1] = (double)st;
+  out[2] = (double)md;
+  out[3] = (double)sd;
+  out[4] = (double)sz;
   diff = df;
 }
 
-// Key list: the same warp-distributed sorted list as TopList, over int keys.
-struct KeyList {
-  int v, id, theta;
-  __device__ __forceinline__ void reset() {
-    v = INT_MIN;
-    id = 0x7fffffff;
-    theta = INT_MIN;
-  }
-  __device__ __forceinline__ bool full(int M) const {
-    return __shfl_sync(0xffffffffu, id, M - 1) != 0x7fffffff;
-  }
-  __device__ __forceinline__ void insert(int cv, int cid, int M, int lane) {
-    const bool beats = lane < M && (v > cv || (v == cv && id < cid));
-    const int pos = __popc(__ballot_sync(0xffffffffu, beats));
-    if (pos < M) {
-      const int uv = __shfl_up_sync(0xffffffffu, v, 1);
-      const int ui = __shfl_up_sync(0xffffffffu, id, 1);
-      if (lane > pos && lane < M) {
-        v = uv;
-        id = ui;
-      }
-      if (lane == pos) {
-        v = cv;
-        id = cid;
-      }
-      theta = __shfl_sync(0xffffffffu, v, M - 1);
-    }
-  }
-};
-
-// Exact top-M of one row, (value desc, id asc) like top_ids (verifier.cpp:40-51),
-// from the per-block maxima the compute warps recorded. theta_b, the M-th
-// largest block maximum, is at most the row's M-th value (the M largest block
-// maxima are M distinct elements), so only blocks whose maximum reaches it
-// and, inside them, only elements >= theta_b can belong to the top M. Those
-// blocks are re-read (L2-resident) and their survivors inserted. Ids past the
-// logical row (ragged-tail padding) never enter.
+// Exact top-M ids of one row, (value desc, id asc) like top_ids
+// (verifier.cpp:40-51). The global top-M blocks (by block maximum) lie in the
+// union of the compute warps' published lists; theta_b, their M-th largest key,
+// is found by a bit-serial radix select (REDUX per step). theta_b is at most the
+// row's M-th value (the M largest block maxima are M distinct elements), so the
+// top M are among the elements >= theta_b of the listed blocks whose key
+// reaches theta_b. Those blocks are re-read (L2-resident), the survivors
+// collected and ranked; ranks < M are the top M. Ids past the logical row
+// (ragged-tail padding) never enter. If ties push more than 128 survivors, a
+// warp-list insertion over the same survivors (exact, slower) takes over.
 template <class In>
-__device__ __noinline__ TopList<typename InTraits<In>::Acc> select_topm(const int *bmax, int nblocks,
-                                                           const In *row, int M, int nlocal,
-                                                           int *cand, int lane) {
+__device__ __noinline__ void select_topm(const int *pub_key, const int *pub_blk, const In *row,
+                                         int M,
+                                         int nlocal, EpiScratch &es, int *sel, int lane) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
-  KeyList K;
-  K.reset();
-  for (int base = 0; base < nblocks; base += 32) {
-    const int bi = base + lane;
-    const int key = bi < nblocks ? bmax[bi] : INT_MIN;
-    unsigned q = __ballot_sync(0xffffffffu, bi < nblocks && key >= K.theta);
-    while (q) {
-      const int src = __ffs(q) - 1;
-      q &= q - 1;
-      const int cv = __shfl_sync(0xffffffffu, key, src);
-      if (cv >= K.theta) K.insert(cv, base + src, M, lane);
-    }
+  constexpr int kT = kCW * kMaxTopM / 32;  // published entries per lane (max)
+  constexpr int kLoads = 16;
+  const int npub = kCW * M;
+  uint32_t u[kT];
+#pragma unroll
+  for (int t = 0; t < kT; ++t) {
+    const int e = t * 32 + lane;
+    u[t] = e < npub ? ((uint32_t)pub_key[e] ^ 0x80000000u) : 0u;
   }
-  const int theta_b = K.full(M) ? K.theta : INT_MIN;
+  uint32_t ans = 0;
+#pragma unroll 1
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t cand = ans | (1u << bit);
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int t = 0; t < kT; ++t) cnt += u[t] >= cand ? 1u : 0u;
+    if (__reduce_add_sync(0xffffffffu, cnt) >= (uint32_t)M) ans = cand;
+  }
+  const int theta_b = (int)(ans ^ 0x80000000u);
   const Acc vb = (Acc)fkey_inv(theta_b);
-  TopList<Acc> L;
+  int nel = 0;
+  bool overflow = false;
+  TopList<Acc> L;  // only used after an overflow
   L.reset();
-  for (int base = 0; base < nblocks; base += 32) {
-    const int bi = base + lane;
-    const bool c = bi < nblocks && bmax[bi] >= theta_b;
-    unsigned q = __ballot_sync(0xffffffffu, c);
-    // gather this batch's candidate blocks, then re-read them 4 at a time
-    int nc = 0;
-    while (q) {
-      const int src = __ffs(q) - 1;
-      q &= q - 1;
-      if (lane == 0) cand[nc] = base + src;
-      ++nc;
-    }
-    __syncwarp();
-    for (int g = 0; g < nc; g += 4) {
-      uint4 raw[4];
-      int id0[4];
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1 && !overflow) break;
+    for (int base = 0; base < npub; base += 32) {
+      const int e = base + lane;
+      const int blk = e < npub ? pub_blk[e] : -1;
+      const bool c = e < npub && blk >= 0 && pub_key[e] >= theta_b;
+      const unsigned q = __ballot_sync(0xffffffffu, c);
+      if (!q) continue;
+      if (c) es.cand[__popc(q & ((1u << lane) - 1u))] = blk;
+      __syncwarp();
+      const int nc = __popc(q);
+      for (int r = 0; r < nc; r += kLoads) {
+        uint4 raw[kLoads];
+        int id0[kLoads];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        id0[k] = -1;
-        raw[k] = make_uint4(0, 0, 0, 0);
-        if (g + k < nc) {
-          const int b = cand[g + k];
-          const int cc = b / (kVecs * kCW), r = b - cc * kVecs * kCW;
-          const int h = r / kCW, w = r - h * kCW;
-          id0[k] = cc * CH + (h * kCT + w * 32 + lane) * VEC;
-          if (id0[k] < nlocal) raw[k] = ldg128(row + id0[k]);
+        for (int k = 0; k < kLoads; ++k) {
+          raw[k] = make_uint4(0, 0, 0, 0);
+          id0[k] = nlocal;
+          if (r + k < nc) {
+            const int b = es.cand[r + k];
+            const int cc = b / (kVecs * kCW), rr = b - cc * kVecs * kCW;
+            const int h = rr / kCW, w = rr - h * kCW;
+            id0[k] = cc * CH + (h * kCT + w * 32 + lane) * VEC;
+            if (id0[k] < nlocal) raw[k] = ldg128(row + id0[k]);
+          }
         }
-      }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (g + k >= nc) break;
-        Acc v[VEC];
-        unpack(raw[k], v, (In *)nullptr);
-        unsigned qm = 0;
+        for (int k = 0; k < kLoads; ++k) {
+          if (r + k >= nc) break;
+          Acc v[VEC];
+          unpack(raw[k], v, (In *)nullptr);
 #pragma unroll
-        for (int e = 0; e < VEC; ++e)
-          if (id0[k] + e < nlocal && v[e] >= vb && v[e] >= L.theta) qm |= 1u << e;
-        unsigned lanes = __ballot_sync(0xffffffffu, qm != 0);
-        while (lanes) {
-          const int src = __ffs(lanes) - 1;
-          lanes &= lanes - 1;
-          unsigned m = __shfl_sync(0xffffffffu, qm, src);
-          const int ib = __shfl_sync(0xffffffffu, id0[k], src);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const Acc cv = __shfl_sync(0xffffffffu, v[e], src);
-            if (((m >> e) & 1u) && cv >= L.theta) L.insert(cv, ib + e, M, lane);
+          for (int ee = 0; ee < VEC; ++ee) {
+            const bool keep = id0[k] + ee < nlocal && v[ee] >= vb;
+            const unsigned kq = __ballot_sync(0xffffffffu, keep);
+            if (pass == 0) {
+              if (keep) {
+                const int slot = nel + __popc(kq & ((1u << lane) - 1u));
+                if (slot < 128) {
+                  es.ev_id[slot] = id0[k] + ee;
+                  es.ev_key[slot] = (double)v[ee];
+                }
+              }
+              nel += __popc(kq);
+            } else {
+              unsigned qq = kq;
+              while (qq) {
+                const int src = __ffs(qq) - 1;
+                qq &= qq - 1;
+                const Acc cv = __shfl_sync(0xffffffffu, v[ee], src);
+                const int ci = __shfl_sync(0xffffffffu, id0[k] + ee, src);
+                if (cv >= L.theta) L.insert(cv, ci, M, lane);
+              }
+            }
           }
         }
       }
+      __syncwarp();
     }
-    __syncwarp();
+    overflow = nel > 128;
   }
-  return L;
+  if (!overflow) {
+    // rank every survivor against the others: (value desc, id asc)
+    for (int i = lane; i < nel; i += 32) {
+      const double vi = es.ev_key[i];
+      const int ii = es.ev_id[i];
+      int rank = 0;
+      for (int k = 0; k < nel; ++k) {
+        const double vk = es.ev_key[k];
+        rank += (vk > vi || (vk == vi && es.ev_id[k] < ii)) ? 1 : 0;
+      }
+      if (rank < M) sel[rank] = ii;
+    }
+  } else if (lane < M) {
+    sel[lane] = L.id;
+  }
+  __syncwarp();
 }
 
 // Exact log-sum-exp of the softened mix (two fp64 passes, one warp) for the
@@ -865,16 +999,19 @@ template <class In>
 __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
                               const In *__restrict__ draft, const In *__restrict__ target,
                               const int32_t *__restrict__ tokens, const DevOut &o,
-                              const DevScratch &s, int ew, int lane) {
+                              const DevScratch &s, int ew, int lane, unsigned long long *tr) {
   using Acc = typename InTraits<In>::Acc;
   const int G1 = p.gamma + 1;
   const int M = p.top_m;
   const double omt_d = (double)p.omt_f, tau_d = (double)p.tau_f;
   const int nblocks = p.n_chunks * kVecs * kCW;
-  int *cand = sm.cand[ew];
+  unsigned long long *trl = lane == 0 ? tr : nullptr;
   for (int n = ew;; n += kEW) {
     const int si = n % kSlots;
+    TR_START(tw);
     mbar_wait(&sm.part_full[si], (n / kSlots) & 1);
+    TR_ADD(trl, kTrEpiWaitFull, tw);
+    TR_START(tx);
     Slot<Acc> &sl = sm.slot[si];
     const int item = sl.item;
     if (item < 0) break;
@@ -888,16 +1025,24 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       double mrg[5];
       int diff = 0;
       merge_partials(sl, p, lane, mrg, diff);
+      TR_ADD(trl, kTrEpiMerge, tx);
+      TR_START(tt);
       int shared = 0;
       if (pair) {
-        const TopList<Acc> Lt = select_topm<In>(sl.u.bmax[0], nblocks, rt, M, p.vocab_local, cand, lane);
-        const TopList<Acc> Ld = select_topm<In>(sl.u.bmax[1], nblocks, rd, M, p.vocab_local, cand, lane);
+        EpiScratch &es = sm.epi[ew];
+        const SlotView sv(sl.area, nblocks, M);
+        select_topm<In>(sv.pkey[0], sv.pblk[0], rt, M, p.vocab_local, es, es.sel[0], lane);
+        select_topm<In>(sv.pkey[1], sv.pblk[1], rd, M, p.vocab_local, es, es.sel[1], lane);
+        const int did = lane < M ? es.sel[1][lane] : -1;
         bool found = false;
-        for (int k = 0; k < M; ++k) found |= (__shfl_sync(0xffffffffu, Lt.id, k) == Ld.id);
+        for (int k = 0; k < M; ++k) found |= (es.sel[0][k] == did);
         shared = __popc(__ballot_sync(0xffffffffu, found && lane < M));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.part_empty[si]);  // partials consumed
+      TR_ADD(trl, kTrEpiTopm, tt);
+      TR_START(td);
+      TR_INC(trl, kTrEpiItems);
 
       PosEval ev;
       if (lane == 0) {
@@ -906,6 +1051,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       }
       const int need_exact = __shfl_sync(0xffffffffu, lane == 0 ? ev.need_exact : 0, 0);
       if (need_exact) {
+        TR_INC(trl, kTrNeedExact);
         const double lse = exact_lse_mix_warp<In>(rt, rd, p.vocab_local, omt_d, tau_d, lane);
         if (lane == 0) {
           if (lse == -INFINITY)
@@ -972,12 +1118,13 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
           }
         }
       }
+      TR_ADD(trl, kTrEpiDecide, td);
     } else {
       // ---- sample item: scan the tile sums for T = u W, resolve the tile ----
       const Request<Acc> &rq = sm.req[sl.req];
       const Weigher<Acc> wf = rq.wf;
       const double u = rq.u;
-      const double *tiles = sl.u.tiles;
+      const double *tiles = reinterpret_cast<const double *>(sl.area);
       double wpart = 0.0;
       for (int t = lane; t < nblocks; t += 32) wpart += tiles[t];
       const double W = warp_sum_f64(wpart);
@@ -1030,6 +1177,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
         }
         complete_item(o, s, p, b);
       }
+      TR_ADD(trl, kTrEpiSample, tx);
     }
     __syncwarp();
     if (lane == 0) {
@@ -1040,14 +1188,16 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
 }
 
 // ------------------------------------------------------------------ producer warp
-template <class In>
-__device__ __forceinline__ void stream_rows(Smem<typename InTraits<In>::Acc> &sm, const In *rt,
+template <class In, class Acc = typename InTraits<In>::Acc>
+__device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
                                             const In *rd, bool two, int item, int kind, int n,
                                             int req, int n_chunks, int nlocal, int &stage,
-                                            uint32_t &phase) {
+                                            uint32_t &phase, unsigned long long *tr) {
   constexpr int CH = kRowBytes / (int)sizeof(In);
   for (int c = 0; c < n_chunks; ++c) {
+    TR_START(tw);
     mbar_wait(&sm.empty[stage], phase ^ 1);
+    TR_ADD(tr, kTrProdWaitEmpty, tw);
     StageMeta m;
     m.item = item;
     m.chunk = c;
@@ -1061,7 +1211,7 @@ __device__ __forceinline__ void stream_rows(Smem<typename InTraits<In>::Acc> &sm
     mbar_arrive_expect_tx(&sm.full[stage], two ? 2u * bytes : bytes);
     bulk_g2s(sm.ring[stage][1], rt + (size_t)c * CH, bytes, &sm.full[stage]);
     if (two) bulk_g2s(sm.ring[stage][0], rd + (size_t)c * CH, bytes, &sm.full[stage]);
-    if (++stage == kStages) {
+    if (++stage == Smem<Acc>::kStages) {
       stage = 0;
       phase ^= 1;
     }
@@ -1071,7 +1221,7 @@ __device__ __forceinline__ void stream_rows(Smem<typename InTraits<In>::Acc> &sm
 template <class In>
 __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
                               const In *__restrict__ draft, const In *__restrict__ target,
-                              const DevScratch &s) {
+                              const DevScratch &s, unsigned long long *tr) {
   const int G1 = p.gamma + 1;
   int stage = 0;
   uint32_t phase = 0;
@@ -1090,7 +1240,9 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       const int j = item / p.B, b = item - j * p.B;
       const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
       const In *rd = draft + ((size_t)b * p.gamma + (j < p.gamma ? j : 0)) * (size_t)p.stride;
-      stream_rows<In>(sm, rt, rd, two, item, kSample, n, r, p.n_chunks, p.vocab_local, stage, phase);
+      stream_rows<In>(sm, rt, rd, two, item, kSample, n, r, p.n_chunks, p.vocab_local, stage, phase,
+                      tr);
+      TR_INC(tr, kTrProdSamples);
       ++n;
       vstore(&sm.req_head, head + 1);
       continue;
@@ -1103,7 +1255,8 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
         const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
         const In *rd = draft + ((size_t)b * p.gamma + (pair ? j : 0)) * (size_t)p.stride;
         stream_rows<In>(sm, rt, rd, pair, item, kRegular, n, 0, p.n_chunks, p.vocab_local, stage,
-                        phase);
+                        phase, tr);
+        TR_INC(tr, kTrProdItems);
         ++n;
         continue;
       }
@@ -1111,12 +1264,14 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
     }
     // drained: wait until the epilogue has seen everything streamed, then
     // re-check for requests it may have posted on the way
+    TR_START(td);
     if (vload(&sm.epi_count) == n) {
       __threadfence_block();
       if (vload(&sm.req_head) == vload(&sm.req_tail)) break;
       continue;
     }
     __nanosleep(256);
+    TR_ADD(tr, kTrProdDrain, td);
   }
   // end of stream
   mbar_wait(&sm.empty[stage], phase ^ 1);
@@ -1141,9 +1296,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   Smem<Acc> &sm = *reinterpret_cast<Smem<Acc> *>(smem_raw);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  unsigned long long *tr = s.trace ? s.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
+  TR_START(tk);
 
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < Smem<Acc>::kStages; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], kCW);
     }
@@ -1159,10 +1316,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   if (warp == kProdWarp) {
-    if (lane == 0) producer_loop<In>(sm, p, draft, target, s);
+    if (lane == 0) producer_loop<In>(sm, p, draft, target, s, tr);
   } else if (warp >= kEpiWarp) {
-    epilogue_loop<In>(sm, p, draft, target, tokens, o, s, warp - kEpiWarp, lane);
+    epilogue_loop<In>(sm, p, draft, target, tokens, o, s, warp - kEpiWarp, lane, tr);
     if (lane == 0 && atomicAdd(&sm.epi_exit, 1) == kEW - 1) {
+      TR_ADD(tr, kTrKernel, tk);
       // last CTA out re-arms the work counters for the next launch
       __threadfence();
       const unsigned prev = atomicAdd(s.exit_count, 1u);
@@ -1174,9 +1332,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     if (p.need_z)
-      compute_loop<In, true>(sm, p, tid);
+      compute_loop<In, true>(sm, p, draft, target, tid, tr);
     else
-      compute_loop<In, false>(sm, p, tid);
+      compute_loop<In, false>(sm, p, draft, target, tid, tr);
   }
 }
 
@@ -1191,7 +1349,9 @@ cudaError_t launch_fused(const DevParams &p, const void *draft, const void *targ
   constexpr int CH = fz::kRowBytes / (int)sizeof(In);
   DevParams q = p;
   q.n_chunks = (p.vocab_local + CH - 1) / CH;
-  if (q.n_chunks * fz::kVecs * fz::kCW > fz::kMaxTiles) return cudaErrorInvalidValue;
+  const int nblocks = q.n_chunks * fz::kVecs * fz::kCW;
+  if (nblocks > fz::kMaxTiles || 8 * nblocks + 16 * fz::kCW * q.top_m > fz::kAreaBytes)
+    return cudaErrorInvalidValue;
   const size_t smem = sizeof(fz::Smem<Acc>);
   // occupancy is a property of (kernel, device): query once per device
   static int cached_device = -1, cached_grid_cap = 0;
@@ -1219,9 +1379,12 @@ cudaError_t launch_fused(const DevParams &p, const void *draft, const void *targ
   return cudaGetLastError();
 }
 
-// Vocabulary limit of the fused kernel for a dtype (sample tiles per slot).
-int fused_max_vocab(int esize) {
-  return fz::kMaxTiles / (fz::kVecs * fz::kCW) * (fz::kRowBytes / esize);
+// Vocabulary limit of the fused kernel for a dtype and top_m (per-slot block
+// maxima + published lists, or sample tiles, must fit the slot area).
+int fused_max_vocab(int esize, int top_m) {
+  const int by_area = (fz::kAreaBytes - 16 * fz::kCW * top_m) / 8;
+  const int nblocks = by_area < fz::kMaxTiles ? by_area : fz::kMaxTiles;
+  return nblocks / (fz::kVecs * fz::kCW) * (fz::kRowBytes / esize);
 }
 
 template cudaError_t launch_fused<__nv_bfloat16>(const DevParams &, const void *, const void *,

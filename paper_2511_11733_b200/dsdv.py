@@ -8,13 +8,15 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libdsdv.so"
+# DSDV_LIB selects an alternate build of the same ABI (e.g. libdsdv_trace.so)
+LIB_PATH = Path(os.environ["DSDV_LIB"]) if os.environ.get("DSDV_LIB") else _PKG / "libdsdv.so"
 
 OK, E_INVARIANT, E_DEGENERATE_MIXTURE, E_DRAFTING_CONTRACT, E_EMPTY_RESIDUAL, E_CUDA, E_NCCL, \
     E_UNSUPPORTED = range(8)
