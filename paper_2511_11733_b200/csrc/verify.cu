@@ -61,7 +61,8 @@ struct Ring {
   static constexpr int kStages = sizeof(Acc) == 8 ? 3 : 4;
 };
 constexpr int kMaxTiles = 2048;      // blocks per slot: (chunk, vector, warp), 32*VEC ids each
-constexpr int kAreaBytes = 20480;    // per-slot block maxima + published lists, or sample tiles
+constexpr int kAreaBytes = 16384;    // per-slot block maxima, or sample tiles
+constexpr int kCap = 256;            // captured top-m candidates per row and item
 constexpr int kReq = 16;             // sample-request queue
 constexpr float kSlack = 8.0f;       // lazy max: rescale when a value exceeds m by this much
 constexpr float kFloorM = -1e30f;    // finite "empty" max (keeps (v - m) free of inf - inf)
@@ -74,7 +75,7 @@ enum TraceWord : int {
   kTrComputeWaitFull = 0, kTrComputeFold, kTrComputeSample, kTrComputeWaitSlot, kTrComputeItemEnd,
   kTrEpiWaitFull, kTrEpiMerge, kTrEpiTopm, kTrEpiDecide, kTrEpiSample, kTrProdWaitEmpty,
   kTrProdDrain, kTrProdItems, kTrProdSamples, kTrKernel, kTrEpiItems, kTrTopmCand, kTrTopmIns,
-  kTrTopmFallback, kTrMaxSurv, kTrNeedExact
+  kTrTopmFallback, kTrMaxSurv, kTrNeedExact, kTrCapCalls, kTrCapLock, kTrCapCycles
 };
 #ifdef DSDV_TRACE
 #define TR_START(v) const long long v = clock64()
@@ -86,10 +87,20 @@ enum TraceWord : int {
   do {                            \
     if (tr) atomicAdd((tr) + (w), 1ull); \
   } while (0)
+#define TR_ACC(tr, w, x)                                       \
+  do {                                                         \
+    if (tr) atomicAdd((tr) + (w), (unsigned long long)(x));    \
+  } while (0)
+#define TR_MAX(tr, w, x)                                       \
+  do {                                                         \
+    if (tr) atomicMax((tr) + (w), (unsigned long long)(x));    \
+  } while (0)
 #else
 #define TR_START(v) (void)0
 #define TR_ADD(tr, w, v) (void)0
 #define TR_INC(tr, w) (void)0
+#define TR_MAX(tr, w, x) (void)0
+#define TR_ACC(tr, w, x) (void)0
 #endif
 
 struct StageMeta {
@@ -102,9 +113,9 @@ struct StageMeta {
 
 template <class Acc>
 struct WarpPartial {
-  Acc mt, st, md, sd, sz;
+  Acc mt, st, md, sd, sz;  // maxima (natural) and sums relative to mtL / mdL
+  Acc mtL, mdL;            // log2 reference points (fl(max * log2 e))
   int diff;
-  int kt[2], kd[2];  // the warp's two largest block keys of each row
 };
 
 template <class Acc>
@@ -113,29 +124,41 @@ struct Slot {
   int kind;
   int req;
   WarpPartial<Acc> wp[kCW];
-  // regular item: per-block max keys of l_t / l_d ([2][nblocks] ints), then each
-  // warp's M largest block keys and block indices ([2][kCW][M] ints, twice);
-  // sample item: per-block weight sums ([nblocks] doubles). See SlotView.
+  // top-m capture per row: per-lane running maxima (capture_row), the bound
+  // theta_run derived from them, and every element that reached theta_run
+  int klist[2][32];
+  int ktheta[2], ncap[2];
+  int cap_id[2][kCap];
+  Acc cap_v[2][kCap];
+  // regular item: per-block max keys of l_t / l_d ([2][nblocks] ints, read only
+  // by the capture-overflow fallback); sample item: per-tile weight sums
+  // ([ntiles] doubles). See SlotView.
   alignas(16) uint8_t area[kAreaBytes];
 };
 
 // Typed views of a slot's area for one launch shape.
 struct SlotView {
   int *bmax[2];
-  int *pkey[2];  // [kCW][M]
-  int *pblk[2];  // [kCW][M]
   double *tiles;
-  __device__ __forceinline__ SlotView(uint8_t *area, int nblocks, int M) {
+  __device__ __forceinline__ SlotView(uint8_t *area, int nblocks) {
     int *a = reinterpret_cast<int *>(area);
     bmax[0] = a;
     bmax[1] = a + nblocks;
-    pkey[0] = a + 2 * nblocks;
-    pkey[1] = pkey[0] + kCW * M;
-    pblk[0] = pkey[1] + kCW * M;
-    pblk[1] = pblk[0] + kCW * M;
     tiles = reinterpret_cast<double *>(area);
   }
 };
+
+// Capture state of a slot back to empty (kernel start, and by the epilogue
+// when it releases a regular item's slot). One warp.
+template <class Acc>
+__device__ __forceinline__ void reset_capture(Slot<Acc> &sl, int lane) {
+  sl.klist[0][lane] = INT_MIN;
+  sl.klist[1][lane] = INT_MIN;
+  if (lane < 2) {
+    sl.ktheta[lane] = INT_MIN;
+    sl.ncap[lane] = 0;
+  }
+}
 
 template <class Acc>
 struct Request {
@@ -195,23 +218,23 @@ constexpr int kKeyNegInf = (int)(0xff800000u ^ 0x7fffffffu);  // fkey(-inf)
 __device__ __forceinline__ int vload(const int *p) { return *(const volatile int *)p; }
 __device__ __forceinline__ void vstore(int *p, int v) { *(volatile int *)p = v; }
 
+// Per-thread online statistics of one item. Sums are relative to log2-scaled
+// reference points mtL = fl(mt * L), mdL = fl(md * L) (L = fp32 log2 e), so an
+// exponent is one FFMA: x = v * L - mtL. The epilogue converts back exactly
+// (lse_from_sum): ln sum 2^(v L) = (mtL + log2 s) ln 2, and the (1.3e-8)
+// relative error of L is corrected to first order with the row maximum.
 template <class Acc>
 struct ItemState {
-  Acc mt, st, md, sd, sz;
+  Acc mt, st, md, sd, sz;  // natural-log maxima (lazy, within kSlack) and sums
+  Acc mtL, mdL;            // log2 reference points of the sums
   uint32_t diff;
-  int kt1, kt2, kd1, kd2;  // warp's two largest block keys per row (warp-uniform)
   __device__ __forceinline__ void reset() {
     mt = md = Acc(kFloorM);
+    mtL = mdL = Acc(kFloorM) * log2e<Acc>();
     st = sd = sz = Acc(0);
     diff = 0;
-    kt1 = kt2 = kd1 = kd2 = INT_MIN;
   }
 };
-
-__device__ __forceinline__ void top2_key(int &k1, int &k2, int key) {
-  k2 = key > k1 ? k1 : (key > k2 ? key : k2);
-  k1 = key > k1 ? key : k1;
-}
 
 __device__ __forceinline__ int warp_max_key(int key) {
   int r;
@@ -220,21 +243,94 @@ __device__ __forceinline__ int warp_max_key(int key) {
 }
 
 // ------------------------------------------------------------------ compute warps
-// Exponent sums of one vector (hot path). fp32: packed f32x2 arithmetic, the
-// softened-mix exponent on the FMA-pipe polynomial (MUFU keeps t and d).
+// Descending bitonic sort of one int per lane.
+__device__ __forceinline__ int warp_sort_desc(int key, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int pk = __shfl_xor_sync(0xffffffffu, key, j);
+      const bool keep_max = ((lane & j) == 0) == ((lane & k) == 0);
+      key = keep_max ? max(key, pk) : min(key, pk);
+    }
+  }
+  return key;
+}
+
+// Top-m capture of one row of one block (chunk c, this warp), taken only when
+// the block's maximum key reaches the row's running bound theta_run
+// (warp-uniform branch; after the first blocks of an item it is rarely taken).
+//
+// Lock-free bound: klist[r][l] holds the largest lane maximum seen so far from
+// lane l of any (chunk, warp) block (shared-memory atomicMax, conflict-free).
+// The 32 entries are distinct elements of the row, so their M-th largest never
+// exceeds the row's M-th largest value: every element of the final top M
+// (top_ids, verifier.cpp:40-51) is >= theta_run when its block streams, and a
+// block whose maximum is below it holds none. The warp folds its lane maxima
+// in, recomputes the bound, and appends its elements >= the bound (ids, values)
+// to the slot's capture buffer; the epilogue ranks only those.
+template <class In>
+__device__ __noinline__ void capture_row(Slot<typename InTraits<In>::Acc> &sl, int r, int lkey,
+                                         const uint8_t *srow, int c, int tid, int lane,
+                                         const DevParams &p, unsigned long long *trl) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int VEC = InTraits<In>::kVec;
+  constexpr int CH = kRowBytes / (int)sizeof(In);
+  TR_START(tc);
+  TR_INC(trl, kTrCapCalls);
+  if (lkey > vload(&sl.klist[r][lane])) atomicMax(&sl.klist[r][lane], lkey);
+  __syncwarp();
+  const int sorted = warp_sort_desc(vload(&sl.klist[r][lane]), lane);
+  const int th = __shfl_sync(0xffffffffu, sorted, p.top_m - 1);
+  if (lane == 0 && th > vload(&sl.ktheta[r])) atomicMax(&sl.ktheta[r], th);
+  // the stage is still resident: re-read this thread's vectors
+  Acc v[kVecs][VEC];
+  unsigned keep = 0;
+  int cnt = 0;
+#pragma unroll
+  for (int h = 0; h < kVecs; ++h) {
+    const int q = h * kCT + tid;
+    unpack(lds128(srow + q * 16), v[h], (In *)nullptr);
+    const int id0 = c * CH + q * VEC;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const bool kp = fkey(v[h][e]) >= th && id0 + e < p.vocab_local;
+      keep |= (kp ? 1u : 0u) << (h * VEC + e);
+      cnt += kp ? 1 : 0;
+    }
+  }
+  if (cnt) {
+    int at = atomicAdd(&sl.ncap[r], cnt);
+#pragma unroll
+    for (int h = 0; h < kVecs; ++h) {
+      const int id0 = c * CH + (h * kCT + tid) * VEC;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if ((keep >> (h * VEC + e)) & 1u) {
+          if (at < kCap) {
+            sl.cap_id[r][at] = id0 + e;
+            sl.cap_v[r][at] = v[h][e];
+          }
+          ++at;
+        }
+    }
+  }
+  TR_ADD(trl, kTrCapCycles, tc);
+}
+
 template <bool PAIR, bool NEEDZ, int VEC>
 __device__ __forceinline__ void exp_sums(const float (&vt)[VEC], const float (&vd)[VEC],
                                          ItemState<float> &S, const DevParams &p) {
   const f32x2 L2 = pk2(kLog2eF, kLog2eF);
-  const f32x2 mt2 = pk2(S.mt, S.mt), md2 = pk2(S.md, S.md);
+  const f32x2 nmt2 = pk2(-S.mtL, -S.mtL), nmd2 = pk2(-S.mdL, -S.mdL);
   const f32x2 omt2 = pk2(p.omt_f, p.omt_f), tau2 = pk2(p.tau_f, p.tau_f);
   f32x2 at = pk2(0.f, 0.f), ad = pk2(0.f, 0.f), az = pk2(0.f, 0.f);
 #pragma unroll
   for (int e = 0; e < VEC; e += 2) {
-    const f32x2 xt = mul2(sub2(pk2(vt[e], vt[e + 1]), mt2), L2);
+    const f32x2 xt = fma2(pk2(vt[e], vt[e + 1]), L2, nmt2);
     at = add2(at, pk2(fast_exp2(lo2(xt)), fast_exp2(hi2(xt))));
     if (PAIR) {
-      const f32x2 xd = mul2(sub2(pk2(vd[e], vd[e + 1]), md2), L2);
+      const f32x2 xd = fma2(pk2(vd[e], vd[e + 1]), L2, nmd2);
       ad = add2(ad, pk2(fast_exp2(lo2(xd)), fast_exp2(hi2(xd))));
       if (NEEDZ) az = add2(az, poly_exp2x2(fma2(omt2, xt, mul2(tau2, xd))));
     }
@@ -253,10 +349,10 @@ __device__ __forceinline__ void exp_sums(const double (&vt)[VEC], const double (
   double at = 0.0, ad = 0.0, az = 0.0;
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {
-    const double xt = (vt[e] - S.mt) * L;
+    const double xt = vt[e] * L - S.mtL;
     at += exp2(xt);
     if (PAIR) {
-      const double xd = (vd[e] - S.md) * L;
+      const double xd = vd[e] * L - S.mdL;
       ad += exp2(xd);
       if (NEEDZ) az += exp2(omt * xt + tau * xd);
     }
@@ -268,79 +364,95 @@ __device__ __forceinline__ void exp_sums(const double (&vt)[VEC], const double (
   }
 }
 
-// Fold one 16-byte vector per row (ids id0..id0+VEC-1; block bi). Top-m
-// bookkeeping is one warp max per vector and row (REDUX) stored as the
-// block's key: the epilogue selects the exact top-m from the few blocks whose
-// maxima can reach it. The only control flow is the warp vote of the (rare)
-// lazy rescale. Called from a rolled loop: the hot loop stays small enough
-// for the instruction caches.
+// Fold this thread's kVecs 16-byte vectors per row of one ring stage (ids of
+// vector h: c*CH + (h*kCT + tid)*VEC + e). Top-m bookkeeping is one warp max
+// per chunk and row (REDUX) — the key of block (chunk, warp) — compared with
+// the row's running bound; the rare blocks that reach it are captured
+// (capture_row). Otherwise the only control flow is the warp vote of the
+// (rare) lazy rescale.
 template <class In, bool PAIR, bool NEEDZ>
-__device__ __forceinline__ void fold_vec(const uint8_t *sdraft, const uint8_t *starget, int q,
-                                         int id0, bool tail, ItemState<typename InTraits<In>::Acc> &S,
-                                         const DevParams &p, int lane, int bi, int *bmax_t,
-                                         int *bmax_d) {
+__device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t *starget, int tid,
+                                           int c, bool tail, ItemState<typename InTraits<In>::Acc> &S,
+                                           const DevParams &p, int warp, int lane,
+                                           Slot<typename InTraits<In>::Acc> &sl, int *bmax_t,
+                                           int *bmax_d, unsigned long long *trl) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
+  constexpr int CH = kRowBytes / (int)sizeof(In);
   const Acc L = log2e<Acc>();
   const Acc ni = neg_inf<Acc>();
 
-  Acc vt[VEC], vd[VEC];
-  const uint4 a = lds128(starget + q * 16);
-  unpack(a, vt, (In *)nullptr);
+  Acc vt[kVecs][VEC], vd[kVecs][VEC];
   uint32_t diff = 0;
-  if (PAIR) {
-    const uint4 bb = lds128(sdraft + q * 16);
-    unpack(bb, vd, (In *)nullptr);
-    diff = (a.x ^ bb.x) | (a.y ^ bb.y) | (a.z ^ bb.z) | (a.w ^ bb.w);
-  } else {
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) vd[e] = Acc(0);
+  for (int h = 0; h < kVecs; ++h) {
+    const int q = h * kCT + tid;
+    const uint4 a = lds128(starget + q * 16);
+    unpack(a, vt[h], (In *)nullptr);
+    if (PAIR) {
+      const uint4 bb = lds128(sdraft + q * 16);
+      unpack(bb, vd[h], (In *)nullptr);
+      diff |= (a.x ^ bb.x) | (a.y ^ bb.y) | (a.z ^ bb.z) | (a.w ^ bb.w);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) vd[h][e] = Acc(0);
+    }
   }
   if (tail) {
     // elements past the logical row are -inf in both rows (no mass, equal,
     // ranked after every real id); the equality flag sees real ids only
     diff = 0;
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      if (id0 + e >= p.vocab_local) {
-        vt[e] = ni;
-        if (PAIR) vd[e] = ni;
-      } else if (PAIR) {
-        diff |= bits_differ(vt[e], vd[e]) ? 1u : 0u;
+    for (int h = 0; h < kVecs; ++h) {
+      const int id0 = c * CH + (h * kCT + tid) * VEC;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        if (id0 + e >= p.vocab_local) {
+          vt[h][e] = ni;
+          if (PAIR) vd[h][e] = ni;
+        } else if (PAIR) {
+          diff |= bits_differ(vt[h][e], vd[h][e]) ? 1u : 0u;
+        }
       }
     }
   }
-  Acc cmt = vt[0];
+  Acc cmt = ni, cmd = ni;
 #pragma unroll
-  for (int e = 1; e < VEC; ++e) cmt = vmax(cmt, vt[e]);
-  Acc cmd = ni;
+  for (int h = 0; h < kVecs; ++h)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      cmt = vmax(cmt, vt[h][e]);
+      if (PAIR) cmd = vmax(cmd, vd[h][e]);
+    }
   if (PAIR) {
     S.diff |= diff;
-    cmd = vd[0];
-#pragma unroll
-    for (int e = 1; e < VEC; ++e) cmd = vmax(cmd, vd[e]);
-    const int bt = warp_max_key(fkey(cmt));
-    const int bd = warp_max_key(fkey(cmd));
-    top2_key(S.kt1, S.kt2, bt);
-    top2_key(S.kd1, S.kd2, bd);
+    const int lt = fkey(cmt), ld = fkey(cmd);
+    const int bt = warp_max_key(lt);
+    const int bd = warp_max_key(ld);
     if (lane == 0) {
-      bmax_t[bi] = bt;
-      bmax_d[bi] = bd;
+      bmax_t[c * kCW + warp] = bt;
+      bmax_d[c * kCW + warp] = bd;
     }
+    if (bt >= vload(&sl.ktheta[0])) capture_row<In>(sl, 0, lt, starget, c, tid, lane, p, trl);
+    if (bd >= vload(&sl.ktheta[1])) capture_row<In>(sl, 1, ld, sdraft, c, tid, lane, p, trl);
   }
-  // lazy online max: one warp vote, rarely taken
+  // lazy online max: one warp vote per chunk, rarely taken
   const bool up_t = cmt > S.mt + Acc(kSlack);
   const bool up_d = PAIR && (cmd > S.md + Acc(kSlack));
   if (__any_sync(0xffffffffu, up_t || up_d)) {
     const Acc nt = up_t ? cmt : S.mt;
     const Acc nd = up_d ? cmd : S.md;
-    if (NEEDZ) S.sz *= fast_exp2((Acc(p.omt_f) * (S.mt - nt) + Acc(p.tau_f) * (S.md - nd)) * L);
-    S.st *= fast_exp2((S.mt - nt) * L);
-    if (PAIR) S.sd *= fast_exp2((S.md - nd) * L);
+    const Acc ntL = nt * L, ndL = nd * L;
+    if (NEEDZ) S.sz *= fast_exp2(Acc(p.omt_f) * (S.mtL - ntL) + Acc(p.tau_f) * (S.mdL - ndL));
+    S.st *= fast_exp2(S.mtL - ntL);
+    if (PAIR) S.sd *= fast_exp2(S.mdL - ndL);
     S.mt = nt;
     S.md = nd;
+    S.mtL = ntL;
+    S.mdL = ndL;
   }
-  exp_sums<PAIR, NEEDZ, VEC>(vt, vd, S, p);
+#pragma unroll
+  for (int h = 0; h < kVecs; ++h) exp_sums<PAIR, NEEDZ, VEC>(vt[h], vd[h], S, p);
 }
 
 // Sample item: per-tile fp64 sums of the residual / bonus weights. Tile
@@ -374,47 +486,6 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
     }
     const double ts = warp_sum_f64((double)ls);
     if (lane == 0) tiles[(chunk * kVecs + h) * kCW + warp] = ts;
-  }
-}
-
-// Item end, per compute warp and row: publish this warp's M largest block
-// keys (and block indices) by M warp-uniform max extractions. The global top-M
-// blocks lie in the union of these lists, so the epilogue never scans all
-// blocks.
-__device__ __forceinline__ void publish_top_blocks(const SlotView &sv, int r, const DevParams &p,
-                                                   int warp, int lane) {
-  const int M = p.top_m;
-  const int nbw = p.n_chunks * kVecs;  // this warp's blocks: i -> (chunk i / kVecs, vector i % kVecs)
-  constexpr int kPer = kMaxTiles / kCW / 32;  // keys per lane (<= 4)
-  int key[kPer];
-#pragma unroll
-  for (int t = 0; t < kPer; ++t) {
-    const int i = t * 32 + lane;
-    key[t] = i < nbw ? sv.bmax[r][((i / kVecs) * kVecs + (i % kVecs)) * kCW + warp] : INT_MIN;
-  }
-  for (int m = 0; m < M; ++m) {
-    int lm = INT_MIN, lt = 0;
-#pragma unroll
-    for (int t = 0; t < kPer; ++t)
-      if (key[t] > lm) {
-        lm = key[t];
-        lt = t;
-      }
-    const int gm = warp_max_key(lm);
-    // lowest lane holding the maximum gives it up (ties leave one at a time)
-    const unsigned own = __ballot_sync(0xffffffffu, lm == gm);
-    const int src = __ffs(own) - 1;
-    const int bi_local = __shfl_sync(0xffffffffu, lt * 32 + lane, src);
-    if (lane == src) {
-#pragma unroll
-      for (int t = 0; t < kPer; ++t)
-        if (t == lt) key[t] = INT_MIN;
-    }
-    if (lane == 0) {
-      sv.pkey[r][warp * M + m] = gm;
-      sv.pblk[r][warp * M + m] =
-          bi_local < nbw ? ((bi_local / kVecs) * kVecs + (bi_local % kVecs)) * kCW + warp : -1;
-    }
   }
 }
 
@@ -465,24 +536,14 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     TR_START(tf);
     if (kind == kRegular) {
       const bool tail = last && (p.vocab_local % CH) != 0;
-      const SlotView sv(sm.slot[s].area, p.n_chunks * kVecs * kCW, p.top_m);
-      int *bt = sv.bmax[0];
-      int *bd = sv.bmax[1];
-      if (pair) {
-#pragma unroll 1
-        for (int h = 0; h < kVecs; ++h) {
-          const int q = h * kCT + tid;
-          fold_vec<In, true, NEEDZ>(sm.ring[stage][0], sm.ring[stage][1], q, c * CH + q * VEC,
-                                    tail, S, p, lane, (c * kVecs + h) * kCW + warp, bt, bd);
-        }
-      } else {
-#pragma unroll 1
-        for (int h = 0; h < kVecs; ++h) {
-          const int q = h * kCT + tid;
-          fold_vec<In, false, false>(sm.ring[stage][0], sm.ring[stage][1], q, c * CH + q * VEC,
-                                     tail, S, p, lane, 0, bt, bd);
-        }
-      }
+      Slot<Acc> &sl = sm.slot[s];
+      const SlotView sv(sl.area, p.n_chunks * kCW);
+      if (pair)
+        fold_chunk<In, true, NEEDZ>(sm.ring[stage][0], sm.ring[stage][1], tid, c, tail, S, p, warp,
+                                    lane, sl, sv.bmax[0], sv.bmax[1], trl);
+      else
+        fold_chunk<In, false, false>(sm.ring[stage][0], sm.ring[stage][1], tid, c, tail, S, p,
+                                     warp, lane, sl, sv.bmax[0], sv.bmax[1], trl);
     } else {
       sample_chunk<In>(sm.ring[stage][0], sm.ring[stage][1], c, sm.req[md.req].wf,
                        reinterpret_cast<double *>(sm.slot[s].area), p, tid, warp, lane);
@@ -500,21 +561,25 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     TR_START(te);
     Slot<Acc> &sl = sm.slot[s];
     if (kind == kRegular) {
-      const Acc omt = Acc(p.omt_f), tau = Acc(p.tau_f), L = log2e<Acc>();
+      const Acc omt = Acc(p.omt_f), tau = Acc(p.tau_f);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         const Acc mt2 = __shfl_xor_sync(0xffffffffu, S.mt, off);
+        const Acc mtL2 = __shfl_xor_sync(0xffffffffu, S.mtL, off);
         const Acc st2 = __shfl_xor_sync(0xffffffffu, S.st, off);
         const Acc md2 = __shfl_xor_sync(0xffffffffu, S.md, off);
+        const Acc mdL2 = __shfl_xor_sync(0xffffffffu, S.mdL, off);
         const Acc sd2 = __shfl_xor_sync(0xffffffffu, S.sd, off);
         const Acc sz2 = __shfl_xor_sync(0xffffffffu, S.sz, off);
-        const Acc Mn = vmax(S.mt, mt2), Dn = vmax(S.md, md2);
-        S.st = S.st * fast_exp2((S.mt - Mn) * L) + st2 * fast_exp2((mt2 - Mn) * L);
-        S.sd = S.sd * fast_exp2((S.md - Dn) * L) + sd2 * fast_exp2((md2 - Dn) * L);
-        S.sz = S.sz * fast_exp2((omt * (S.mt - Mn) + tau * (S.md - Dn)) * L) +
-               sz2 * fast_exp2((omt * (mt2 - Mn) + tau * (md2 - Dn)) * L);
-        S.mt = Mn;
-        S.md = Dn;
+        const Acc ML = vmax(S.mtL, mtL2), DL = vmax(S.mdL, mdL2);
+        S.st = S.st * fast_exp2(S.mtL - ML) + st2 * fast_exp2(mtL2 - ML);
+        S.sd = S.sd * fast_exp2(S.mdL - DL) + sd2 * fast_exp2(mdL2 - DL);
+        S.sz = S.sz * fast_exp2(omt * (S.mtL - ML) + tau * (S.mdL - DL)) +
+               sz2 * fast_exp2(omt * (mtL2 - ML) + tau * (mdL2 - DL));
+        S.mt = vmax(S.mt, mt2);
+        S.md = vmax(S.md, md2);
+        S.mtL = ML;
+        S.mdL = DL;
       }
       const int anydiff = __any_sync(0xffffffffu, S.diff != 0);
       if (lane == 0) {
@@ -524,19 +589,12 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
         w.md = S.md;
         w.sd = S.sd;
         w.sz = S.sz;
+        w.mtL = S.mtL;
+        w.mdL = S.mdL;
         w.diff = anydiff;
-        w.kt[0] = S.kt1;
-        w.kt[1] = S.kt2;
-        w.kd[0] = S.kd1;
-        w.kd[1] = S.kd2;
         sl.wp[warp] = w;
       }
       S.reset();
-      if (pair) {
-        const SlotView sv(sl.area, p.n_chunks * kVecs * kCW, p.top_m);
-        publish_top_blocks(sv, 0, p, warp, lane);
-        publish_top_blocks(sv, 1, p, warp, lane);
-      }
     }
     if (tid == 0) {
       sl.item = md.item;
@@ -551,12 +609,14 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
 
 // ------------------------------------------------------------------ epilogue warp
 // Merge of the kCW warp partials (lanes 0..kCW-1, xor tree) in the
-// accumulation precision, widened to fp64 at the end.
+// accumulation precision. out = {mt, st, md, sd, sz, mtL, mdL}: maxima
+// (natural), sums relative to the log2 reference points mtL / mdL (and
+// (1-tau) mtL + tau mdL for sz).
 template <class Acc>
 __device__ __noinline__ void merge_partials(const Slot<Acc> &sl, const DevParams &p, int lane,
-                                            double (&out)[5], int &diff) {
-  const Acc L = log2e<Acc>();
-  Acc mt = Acc(kFloorM), st = Acc(0), md = Acc(kFloorM), sd = Acc(0), sz = Acc(0);
+                                            double (&out)[7], int &diff) {
+  Acc mt = Acc(kFloorM), md = Acc(kFloorM), st = Acc(0), sd = Acc(0), sz = Acc(0);
+  Acc mtL = Acc(kFloorM) * log2e<Acc>(), mdL = mtL;
   int df = 0;
   if (lane < kCW) {
     const WarpPartial<Acc> w = sl.wp[lane];
@@ -565,150 +625,153 @@ __device__ __noinline__ void merge_partials(const Slot<Acc> &sl, const DevParams
     md = w.md;
     sd = w.sd;
     sz = w.sz;
+    mtL = w.mtL;
+    mdL = w.mdL;
     df = w.diff;
   }
   const Acc omt = Acc(p.omt_f), tau = Acc(p.tau_f);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const Acc mt2 = __shfl_xor_sync(0xffffffffu, mt, off);
-    const Acc st2 = __shfl_xor_sync(0xffffffffu, st, off);
     const Acc md2 = __shfl_xor_sync(0xffffffffu, md, off);
+    const Acc mtL2 = __shfl_xor_sync(0xffffffffu, mtL, off);
+    const Acc mdL2 = __shfl_xor_sync(0xffffffffu, mdL, off);
+    const Acc st2 = __shfl_xor_sync(0xffffffffu, st, off);
     const Acc sd2 = __shfl_xor_sync(0xffffffffu, sd, off);
     const Acc sz2 = __shfl_xor_sync(0xffffffffu, sz, off);
     df |= __shfl_xor_sync(0xffffffffu, df, off);
-    const Acc Mn = vmax(mt, mt2), Dn = vmax(md, md2);
-    st = st * fast_exp2((mt - Mn) * L) + st2 * fast_exp2((mt2 - Mn) * L);
-    sd = sd * fast_exp2((md - Dn) * L) + sd2 * fast_exp2((md2 - Dn) * L);
-    sz = sz * fast_exp2((omt * (mt - Mn) + tau * (md - Dn)) * L) +
-         sz2 * fast_exp2((omt * (mt2 - Mn) + tau * (md2 - Dn)) * L);
-    mt = Mn;
-    md = Dn;
+    const Acc ML = vmax(mtL, mtL2), DL = vmax(mdL, mdL2);
+    st = st * fast_exp2(mtL - ML) + st2 * fast_exp2(mtL2 - ML);
+    sd = sd * fast_exp2(mdL - DL) + sd2 * fast_exp2(mdL2 - DL);
+    sz = sz * fast_exp2(omt * (mtL - ML) + tau * (mdL - DL)) +
+         sz2 * fast_exp2(omt * (mtL2 - ML) + tau * (mdL2 - DL));
+    mt = vmax(mt, mt2);
+    md = vmax(md, md2);
+    mtL = ML;
+    mdL = DL;
   }
   out[0] = (double)mt;
   out[1] = (double)st;
   out[2] = (double)md;
   out[3] = (double)sd;
   out[4] = (double)sz;
+  out[5] = (double)mtL;
+  out[6] = (double)mdL;
   diff = df;
 }
 
 // Exact top-M ids of one row, (value desc, id asc) like top_ids
-// (verifier.cpp:40-51). The global top-M blocks (by block maximum) lie in the
-// union of the compute warps' published lists; theta_b, their M-th largest key,
-// is found by a bit-serial radix select (REDUX per step). theta_b is at most the
-// row's M-th value (the M largest block maxima are M distinct elements), so the
-// top M are among the elements >= theta_b of the listed blocks whose key
-// reaches theta_b. Those blocks are re-read (L2-resident), the survivors
-// collected and ranked; ranks < M are the top M. Ids past the logical row
-// (ragged-tail padding) never enter. If ties push more than 128 survivors, a
-// warp-list insertion over the same survivors (exact, slower) takes over.
+// (verifier.cpp:40-51), from the compute warps' capture (capture_row): the
+// captured elements whose key reaches the final theta_run are a superset of the
+// top M; they are collected and each ranked against the others (ranks < M are
+// the top M). If ties push more than 128 survivors past theta_run, a warp-list
+// insertion over the capture takes over; if the capture buffer itself
+// overflowed (e.g. rows sorted by id), the listed blocks whose maximum reaches
+// theta_run are re-read. Both fallbacks are exact, only slower.
 template <class In>
-__device__ __noinline__ void select_topm(const int *pub_key, const int *pub_blk, const In *row,
-                                         int M,
-                                         int nlocal, EpiScratch &es, int *sel, int lane) {
+__device__ __noinline__ void select_topm(const Slot<typename InTraits<In>::Acc> &sl, int r,
+                                         const int *bmax, int nblocks, const In *row, int M,
+                                         int nlocal, EpiScratch &es, int *sel, int lane,
+                                         unsigned long long *trl) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
-  constexpr int kT = kCW * kMaxTopM / 32;  // published entries per lane (max)
-  constexpr int kLoads = 16;
-  const int npub = kCW * M;
-  uint32_t u[kT];
-#pragma unroll
-  for (int t = 0; t < kT; ++t) {
-    const int e = t * 32 + lane;
-    u[t] = e < npub ? ((uint32_t)pub_key[e] ^ 0x80000000u) : 0u;
+  const int th = vload(&sl.ktheta[r]);
+  const int ncap = vload(&sl.ncap[r]);
+  TR_ACC(trl, kTrTopmCand, ncap);
+  if (ncap <= kCap) {
+    int nel = 0;
+    for (int base = 0; base < ncap; base += 32) {
+      const int i = base + lane;
+      Acc v = Acc(0);
+      int id = 0;
+      bool keep = false;
+      if (i < ncap) {
+        v = sl.cap_v[r][i];
+        id = sl.cap_id[r][i];
+        keep = fkey(v) >= th;
+      }
+      const unsigned q = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int at = nel + __popc(q & ((1u << lane) - 1u));
+        if (at < 128) {
+          es.ev_id[at] = id;
+          es.ev_key[at] = (double)v;
+        }
+      }
+      nel += __popc(q);
+    }
+    __syncwarp();
+    TR_MAX(trl, kTrMaxSurv, nel);
+    if (nel <= 128) {
+      // rank every survivor against the others: (value desc, id asc)
+      for (int i = lane; i < nel; i += 32) {
+        const double vi = es.ev_key[i];
+        const int ii = es.ev_id[i];
+        int rank = 0;
+        for (int k = 0; k < nel; ++k) {
+          const double vk = es.ev_key[k];
+          rank += (vk > vi || (vk == vi && es.ev_id[k] < ii)) ? 1 : 0;
+        }
+        if (rank < M) sel[rank] = ii;
+      }
+      __syncwarp();
+      return;
+    }
+    TR_INC(trl, kTrTopmFallback);
+    TopList<Acc> L;
+    L.reset();
+    for (int base = 0; base < ncap; base += 32) {
+      const int i = base + lane;
+      const Acc v = i < ncap ? sl.cap_v[r][i] : neg_inf<Acc>();
+      const int id = i < ncap ? sl.cap_id[r][i] : 0;
+      unsigned q = __ballot_sync(0xffffffffu, i < ncap && fkey(v) >= th && v >= L.theta);
+      while (q) {
+        const int src = __ffs(q) - 1;
+        q &= q - 1;
+        const Acc cv = __shfl_sync(0xffffffffu, v, src);
+        const int ci = __shfl_sync(0xffffffffu, id, src);
+        if (cv >= L.theta) L.insert(cv, ci, M, lane);
+      }
+    }
+    if (lane < M) sel[lane] = L.id;
+    __syncwarp();
+    return;
   }
-  uint32_t ans = 0;
-#pragma unroll 1
-  for (int bit = 31; bit >= 0; --bit) {
-    const uint32_t cand = ans | (1u << bit);
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int t = 0; t < kT; ++t) cnt += u[t] >= cand ? 1u : 0u;
-    if (__reduce_add_sync(0xffffffffu, cnt) >= (uint32_t)M) ans = cand;
-  }
-  const int theta_b = (int)(ans ^ 0x80000000u);
-  const Acc vb = (Acc)fkey_inv(theta_b);
-  int nel = 0;
-  bool overflow = false;
-  TopList<Acc> L;  // only used after an overflow
+  // capture overflow: re-read every block whose maximum reaches theta_run
+  TR_INC(trl, kTrTopmFallback);
+  TopList<Acc> L;
   L.reset();
-  for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 1 && !overflow) break;
-    for (int base = 0; base < npub; base += 32) {
-      const int e = base + lane;
-      const int blk = e < npub ? pub_blk[e] : -1;
-      const bool c = e < npub && blk >= 0 && pub_key[e] >= theta_b;
-      const unsigned q = __ballot_sync(0xffffffffu, c);
-      if (!q) continue;
-      if (c) es.cand[__popc(q & ((1u << lane) - 1u))] = blk;
-      __syncwarp();
-      const int nc = __popc(q);
-      for (int r = 0; r < nc; r += kLoads) {
-        uint4 raw[kLoads];
-        int id0[kLoads];
+  for (int b0 = 0; b0 < nblocks; b0 += 32) {
+    const int bi = b0 + lane;
+    unsigned q = __ballot_sync(0xffffffffu, bi < nblocks && bmax[bi] >= th);
+    while (q) {
+      const int blk = b0 + __ffs(q) - 1;
+      q &= q - 1;
+      const int cc = blk / kCW, w = blk - cc * kCW;
+#pragma unroll 1
+      for (int h = 0; h < kVecs; ++h) {
+        const int id0 = cc * CH + (h * kCT + w * 32 + lane) * VEC;
+        Acc v[VEC];
 #pragma unroll
-        for (int k = 0; k < kLoads; ++k) {
-          raw[k] = make_uint4(0, 0, 0, 0);
-          id0[k] = nlocal;
-          if (r + k < nc) {
-            const int b = es.cand[r + k];
-            const int cc = b / (kVecs * kCW), rr = b - cc * kVecs * kCW;
-            const int h = rr / kCW, w = rr - h * kCW;
-            id0[k] = cc * CH + (h * kCT + w * 32 + lane) * VEC;
-            if (id0[k] < nlocal) raw[k] = ldg128(row + id0[k]);
-          }
-        }
+        for (int e = 0; e < VEC; ++e) v[e] = neg_inf<Acc>();
+        if (id0 < nlocal) unpack(ldg128(row + id0), v, (In *)nullptr);
 #pragma unroll
-        for (int k = 0; k < kLoads; ++k) {
-          if (r + k >= nc) break;
-          Acc v[VEC];
-          unpack(raw[k], v, (In *)nullptr);
-#pragma unroll
-          for (int ee = 0; ee < VEC; ++ee) {
-            const bool keep = id0[k] + ee < nlocal && v[ee] >= vb;
-            const unsigned kq = __ballot_sync(0xffffffffu, keep);
-            if (pass == 0) {
-              if (keep) {
-                const int slot = nel + __popc(kq & ((1u << lane) - 1u));
-                if (slot < 128) {
-                  es.ev_id[slot] = id0[k] + ee;
-                  es.ev_key[slot] = (double)v[ee];
-                }
-              }
-              nel += __popc(kq);
-            } else {
-              unsigned qq = kq;
-              while (qq) {
-                const int src = __ffs(qq) - 1;
-                qq &= qq - 1;
-                const Acc cv = __shfl_sync(0xffffffffu, v[ee], src);
-                const int ci = __shfl_sync(0xffffffffu, id0[k] + ee, src);
-                if (cv >= L.theta) L.insert(cv, ci, M, lane);
-              }
-            }
+        for (int e = 0; e < VEC; ++e) {
+          const bool c = id0 + e < nlocal && fkey(v[e]) >= th && v[e] >= L.theta;
+          unsigned qq = __ballot_sync(0xffffffffu, c);
+          while (qq) {
+            const int src = __ffs(qq) - 1;
+            qq &= qq - 1;
+            const Acc cv = __shfl_sync(0xffffffffu, v[e], src);
+            const int ci = __shfl_sync(0xffffffffu, id0 + e, src);
+            if (cv >= L.theta) L.insert(cv, ci, M, lane);
           }
         }
       }
-      __syncwarp();
     }
-    overflow = nel > 128;
   }
-  if (!overflow) {
-    // rank every survivor against the others: (value desc, id asc)
-    for (int i = lane; i < nel; i += 32) {
-      const double vi = es.ev_key[i];
-      const int ii = es.ev_id[i];
-      int rank = 0;
-      for (int k = 0; k < nel; ++k) {
-        const double vk = es.ev_key[k];
-        rank += (vk > vi || (vk == vi && es.ev_id[k] < ii)) ? 1 : 0;
-      }
-      if (rank < M) sel[rank] = ii;
-    }
-  } else if (lane < M) {
-    sel[lane] = L.id;
-  }
+  if (lane < M) sel[lane] = L.id;
   __syncwarp();
 }
 
@@ -746,14 +809,20 @@ __device__ __noinline__ double exact_lse_mix_warp(const In *rt, const In *rd, in
 // :112-117, norm_match :119-134, is_key :136-159, effective distribution
 // :231-233 with soften's short-circuits :170-172).
 template <class In>
-__device__ __noinline__ void evaluate_position(const double (&mrg)[5], int diff, int shared,
+__device__ __noinline__ void evaluate_position(const double (&mrg)[7], int diff, int shared,
                                                const DevParams &p, const In *rt, const In *rd,
                                                int y, bool pair, PosEval &ev) {
+  using Acc = typename InTraits<In>::Acc;
   const double Mt = mrg[0], St = mrg[1], Md = mrg[2], Sd = mrg[3], Sz = mrg[4];
+  const double MtL = mrg[5], MdL = mrg[6];
+  // sum 2^(v L - mL) = sum e^(v (1 + d)) e^(-mL ln2) with 1 + d = L ln 2; the
+  // first-order correction of d uses the row maximum for E_P[v].
+  const double d = (double)log2e<Acc>() * kLn2 - 1.0;
+  const double omt = (double)p.omt_f, tau = (double)p.tau_f;
   ev.mt = Mt;
-  ev.lst = log(St);
+  ev.lst = (MtL + log2(St)) * kLn2 - d * Mt - Mt;
   ev.md = Md;
-  ev.lsd = pair ? log(Sd) : 0.0;
+  ev.lsd = pair ? (MdL + log2(Sd)) * kLn2 - d * Md - Md : 0.0;
   ev.lsz = 0.0;
   ev.err = 0;
   ev.key = 0;
@@ -803,10 +872,12 @@ __device__ __noinline__ void evaluate_position(const double (&mrg)[5], int diff,
   else
     ev.kind = DSDV_EFF_SOFTENED;
   if (ev.kind == DSDV_EFF_SOFTENED && !ev.err) {
-    if (Sz > 1e-30 && isfinite(Sz))
-      ev.lsz = log(Sz);
-    else
+    if (Sz > 1e-30 && isfinite(Sz)) {
+      const double zL = omt * MtL + tau * MdL, z = omt * Mt + tau * Md;
+      ev.lsz = (zL + log2(Sz)) * kLn2 - d * z - z;
+    } else {
       ev.need_exact = 1;
+    }
   }
 }
 
@@ -1022,7 +1093,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
     int2 *slotp = s.slots + (size_t)b * G1 + j;
 
     if (sl.kind == kRegular) {
-      double mrg[5];
+      double mrg[7];
       int diff = 0;
       merge_partials(sl, p, lane, mrg, diff);
       TR_ADD(trl, kTrEpiMerge, tx);
@@ -1030,9 +1101,11 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       int shared = 0;
       if (pair) {
         EpiScratch &es = sm.epi[ew];
-        const SlotView sv(sl.area, nblocks, M);
-        select_topm<In>(sv.pkey[0], sv.pblk[0], rt, M, p.vocab_local, es, es.sel[0], lane);
-        select_topm<In>(sv.pkey[1], sv.pblk[1], rd, M, p.vocab_local, es, es.sel[1], lane);
+        const int nb = p.n_chunks * kCW;
+        const SlotView sv(sl.area, nb);
+        select_topm<In>(sl, 0, sv.bmax[0], nb, rt, M, p.vocab_local, es, es.sel[0], lane, trl);
+        select_topm<In>(sl, 1, sv.bmax[1], nb, rd, M, p.vocab_local, es, es.sel[1], lane, trl);
+        reset_capture(sl, lane);
         const int did = lane < M ? es.sel[1][lane] : -1;
         bool found = false;
         for (int k = 0; k < M; ++k) found |= (es.sel[0][k] == did);
@@ -1313,6 +1386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kReq; ++i) sm.req[i].ready = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (warp < kSlots) reset_capture(sm.slot[warp], lane);
   __syncthreads();
 
   if (warp == kProdWarp) {
@@ -1349,8 +1423,8 @@ cudaError_t launch_fused(const DevParams &p, const void *draft, const void *targ
   constexpr int CH = fz::kRowBytes / (int)sizeof(In);
   DevParams q = p;
   q.n_chunks = (p.vocab_local + CH - 1) / CH;
-  const int nblocks = q.n_chunks * fz::kVecs * fz::kCW;
-  if (nblocks > fz::kMaxTiles || 8 * nblocks + 16 * fz::kCW * q.top_m > fz::kAreaBytes)
+  const int ntiles = q.n_chunks * fz::kVecs * fz::kCW;
+  if (ntiles > fz::kMaxTiles || 8 * q.n_chunks * fz::kCW > fz::kAreaBytes)
     return cudaErrorInvalidValue;
   const size_t smem = sizeof(fz::Smem<Acc>);
   // occupancy is a property of (kernel, device): query once per device
@@ -1379,12 +1453,14 @@ cudaError_t launch_fused(const DevParams &p, const void *draft, const void *targ
   return cudaGetLastError();
 }
 
-// Vocabulary limit of the fused kernel for a dtype and top_m (per-slot block
-// maxima + published lists, or sample tiles, must fit the slot area).
+// Vocabulary limit of the fused kernel for a dtype (per-slot block maxima, or
+// sample tiles, must fit the slot area).
 int fused_max_vocab(int esize, int top_m) {
-  const int by_area = (fz::kAreaBytes - 16 * fz::kCW * top_m) / 8;
-  const int nblocks = by_area < fz::kMaxTiles ? by_area : fz::kMaxTiles;
-  return nblocks / (fz::kVecs * fz::kCW) * (fz::kRowBytes / esize);
+  (void)top_m;
+  const int by_tiles = fz::kMaxTiles / (fz::kVecs * fz::kCW);
+  const int by_area = fz::kAreaBytes / (8 * fz::kCW);
+  const int chunks = by_tiles < by_area ? by_tiles : by_area;
+  return chunks * (fz::kRowBytes / esize);
 }
 
 template cudaError_t launch_fused<__nv_bfloat16>(const DevParams &, const void *, const void *,

@@ -19,7 +19,8 @@ from paper_2511_11733_b200.dsdv import Verifier, VerifyParams, WindowResult  # n
 names = ["compute_wait_full", "compute_fold", "compute_sample", "compute_wait_slot",
          "compute_item_end", "epi_wait_full", "epi_merge", "epi_topm", "epi_decide", "epi_sample",
          "prod_wait_empty", "prod_drain", "prod_items", "prod_samples", "kernel", "epi_items",
-         "topm_candidates", "topm_survivors", "topm_fallbacks", "max_survivors", "need_exact"]
+         "topm_candidates", "topm_survivors", "topm_fallbacks", "max_survivors", "need_exact",
+         "cap_calls", "compute_cap_lock", "compute_cap"]
 B = int(os.environ.get("B", 256))
 V = int(os.environ.get("V", 128256))
 G = int(os.environ.get("G", 8))
@@ -60,7 +61,7 @@ for i, n in enumerate(names):
         res[n] = float(t[:, i].max())
         continue
     if n in ("prod_items", "prod_samples", "epi_items", "kernel", "topm_candidates",
-             "topm_survivors", "topm_fallbacks", "need_exact"):
+             "topm_survivors", "topm_fallbacks", "need_exact", "cap_calls"):
         res[n] = t[:, i].sum() / reps
         continue
     per = {"compute": 16, "epi": 2, "prod": 1}[n.split("_")[0]]
