@@ -242,11 +242,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   uint32_t done = 0;
   const uint32_t a = smem_addr(bar);
   do {
+    // the suspend-time hint parks the warp in hardware until the phase flips,
+    // instead of re-issuing the probe (spinning warps steal issue slots from
+    // the compute warps)
     asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
-        "p; }"
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, "
+        "0, p; }"
         : "=r"(done)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(0x989680u)
         : "memory");
   } while (!done);
 }

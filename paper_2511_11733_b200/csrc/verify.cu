@@ -103,12 +103,13 @@ enum TraceWord : int {
 #define TR_ACC(tr, w, x) (void)0
 #endif
 
-struct StageMeta {
+struct alignas(16) StageMeta {  // one LDS.128 per chunk
   int item;   // global item id (b, j), -1 = end of stream
   int chunk;
-  int kind;   // kRegular / kSample
   int n;      // CTA-local stream index (slot = n % kSlots)
-  int req;    // sample request index
+  int kr;     // kind (kRegular / kSample) | sample request index << 1
+  __device__ __forceinline__ int kind() const { return kr & 1; }
+  __device__ __forceinline__ int req() const { return kr >> 1; }
 };
 
 template <class Acc>
@@ -202,6 +203,12 @@ __device__ __forceinline__ bool bits_differ(double a, double b) {
 }
 __device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ float vmax3(float a, float b, float c) {  // FMNMX3
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ double vmax3(double a, double b, double c) { return fmax(fmax(a, b), c); }
 
 // Order-preserving int key of a float (shared-memory atomicMax of thresholds).
 __device__ __forceinline__ int fkey(float f) {
@@ -257,61 +264,73 @@ __device__ __forceinline__ int warp_sort_desc(int key, int lane) {
   return key;
 }
 
-// Top-m capture of one row of one block (chunk c, this warp), taken only when
-// the block's maximum key reaches the row's running bound theta_run
-// (warp-uniform branch; after the first blocks of an item it is rarely taken).
-//
-// Lock-free bound: klist[r][l] holds the largest lane maximum seen so far from
+// ---- top-m capture (top_ids, verifier.cpp:40-51) ----
+// Per slot and row, klist[r][l] holds the largest lane maximum seen so far from
 // lane l of any (chunk, warp) block (shared-memory atomicMax, conflict-free).
 // The 32 entries are distinct elements of the row, so their M-th largest never
-// exceeds the row's M-th largest value: every element of the final top M
-// (top_ids, verifier.cpp:40-51) is >= theta_run when its block streams, and a
-// block whose maximum is below it holds none. The warp folds its lane maxima
-// in, recomputes the bound, and appends its elements >= the bound (ids, values)
-// to the slot's capture buffer; the epilogue ranks only those.
+// exceeds the row's M-th largest value; theta_run (ktheta) is a value that is
+// at most that. Every element of the final top M is >= theta_run when its
+// block streams, and a block whose maximum is below theta_run holds none of
+// them. The compute warps append the elements that reach theta_run (ids,
+// values) to the slot's capture buffer; the epilogue ranks only those.
+
+// M-th largest of the 32 bins of a row (one warp, bitonic sort).
+__device__ __noinline__ int theta_from_bins(const int *bins, int M, int lane) {
+  const int sorted = warp_sort_desc(vload(bins + lane), lane);
+  return __shfl_sync(0xffffffffu, sorted, M - 1);
+}
+
+// key(v) >= th  <=>  v >= fkey_inv(th) (keys round toward -inf)
+template <class Acc>
+__device__ __forceinline__ Acc key_floor(int th) {
+  return th == INT_MIN ? neg_inf<Acc>() : (Acc)fkey_inv(th);
+}
+
+// Rare path of a block whose maximum reached theta_run (out of line; the
+// stage is still resident, so the values are re-read from shared memory):
+// fold the lane maxima into the bins, raise theta_run when at least M + 2 bins
+// lie above it (one sort), and capture the elements that reach it — only the
+// lanes whose maximum reaches the bound look at their elements.
 template <class In>
 __device__ __noinline__ void capture_row(Slot<typename InTraits<In>::Acc> &sl, int r, int lkey,
-                                         const uint8_t *srow, int c, int tid, int lane,
-                                         const DevParams &p, unsigned long long *trl) {
+                                         const uint8_t *srow, int id_base, int M, int nlocal,
+                                         int lane, unsigned long long *trl) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
-  constexpr int CH = kRowBytes / (int)sizeof(In);
   TR_START(tc);
   TR_INC(trl, kTrCapCalls);
-  if (lkey > vload(&sl.klist[r][lane])) atomicMax(&sl.klist[r][lane], lkey);
-  __syncwarp();
-  const int sorted = warp_sort_desc(vload(&sl.klist[r][lane]), lane);
-  const int th = __shfl_sync(0xffffffffu, sorted, p.top_m - 1);
-  if (lane == 0 && th > vload(&sl.ktheta[r])) atomicMax(&sl.ktheta[r], th);
-  // the stage is still resident: re-read this thread's vectors
-  Acc v[kVecs][VEC];
-  unsigned keep = 0;
-  int cnt = 0;
-#pragma unroll
-  for (int h = 0; h < kVecs; ++h) {
-    const int q = h * kCT + tid;
-    unpack(lds128(srow + q * 16), v[h], (In *)nullptr);
-    const int id0 = c * CH + q * VEC;
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      const bool kp = fkey(v[h][e]) >= th && id0 + e < p.vocab_local;
-      keep |= (kp ? 1u : 0u) << (h * VEC + e);
-      cnt += kp ? 1 : 0;
+  int *bins = sl.klist[r];
+  int bin = vload(bins + lane);
+  if (lkey > bin) {
+    atomicMax(bins + lane, lkey);
+    bin = lkey;  // at least
+  }
+  int th = vload(&sl.ktheta[r]);
+  if (__popc(__ballot_sync(0xffffffffu, bin > th)) >= M + 2) {
+    TR_INC(trl, kTrCapLock);
+    __syncwarp();
+    const int nth = theta_from_bins(bins, M, lane);
+    if (nth > th) {
+      th = nth;
+      if (lane == 0) atomicMax(&sl.ktheta[r], nth);
     }
   }
-  if (cnt) {
-    int at = atomicAdd(&sl.ncap[r], cnt);
-#pragma unroll
+  if (lkey >= th) {
+    const Acc thv = key_floor<Acc>(th);
+#pragma unroll 1
     for (int h = 0; h < kVecs; ++h) {
-      const int id0 = c * CH + (h * kCT + tid) * VEC;
+      const int q = h * kCT;  // + tid folded into srow / id_base
+      Acc v[VEC];
+      unpack(lds128(srow + q * 16), v, (In *)nullptr);
+      const int id0 = id_base + q * VEC;
 #pragma unroll
       for (int e = 0; e < VEC; ++e)
-        if ((keep >> (h * VEC + e)) & 1u) {
+        if (v[e] >= thv && id0 + e < nlocal) {
+          const int at = atomicAdd(&sl.ncap[r], 1);
           if (at < kCap) {
             sl.cap_id[r][at] = id0 + e;
-            sl.cap_v[r][at] = v[h][e];
+            sl.cap_v[r][at] = v[e];
           }
-          ++at;
         }
     }
   }
@@ -370,9 +389,9 @@ __device__ __forceinline__ void exp_sums(const double (&vt)[VEC], const double (
 // the row's running bound; the rare blocks that reach it are captured
 // (capture_row). Otherwise the only control flow is the warp vote of the
 // (rare) lazy rescale.
-template <class In, bool PAIR, bool NEEDZ>
+template <class In, bool PAIR, bool NEEDZ, bool TAIL>
 __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t *starget, int tid,
-                                           int c, bool tail, ItemState<typename InTraits<In>::Acc> &S,
+                                           int c, ItemState<typename InTraits<In>::Acc> &S,
                                            const DevParams &p, int warp, int lane,
                                            Slot<typename InTraits<In>::Acc> &sl, int *bmax_t,
                                            int *bmax_d, unsigned long long *trl) {
@@ -398,7 +417,7 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
       for (int e = 0; e < VEC; ++e) vd[h][e] = Acc(0);
     }
   }
-  if (tail) {
+  if (TAIL) {
     // elements past the logical row are -inf in both rows (no mass, equal,
     // ranked after every real id); the equality flag sees real ids only
     diff = 0;
@@ -420,9 +439,9 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
 #pragma unroll
   for (int h = 0; h < kVecs; ++h)
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      cmt = vmax(cmt, vt[h][e]);
-      if (PAIR) cmd = vmax(cmd, vd[h][e]);
+    for (int e = 0; e < VEC; e += 2) {
+      cmt = vmax3(cmt, vt[h][e], vt[h][e + 1]);
+      if (PAIR) cmd = vmax3(cmd, vd[h][e], vd[h][e + 1]);
     }
   if (PAIR) {
     S.diff |= diff;
@@ -433,8 +452,13 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
       bmax_t[c * kCW + warp] = bt;
       bmax_d[c * kCW + warp] = bd;
     }
-    if (bt >= vload(&sl.ktheta[0])) capture_row<In>(sl, 0, lt, starget, c, tid, lane, p, trl);
-    if (bd >= vload(&sl.ktheta[1])) capture_row<In>(sl, 1, ld, sdraft, c, tid, lane, p, trl);
+    // this thread's first vector: byte tid*16 of the stage, id c*CH + tid*VEC
+    if (bt >= vload(&sl.ktheta[0]))
+      capture_row<In>(sl, 0, lt, starget + tid * 16, c * CH + tid * VEC, p.top_m, p.vocab_local,
+                      lane, trl);
+    if (bd >= vload(&sl.ktheta[1]))
+      capture_row<In>(sl, 1, ld, sdraft + tid * 16, c * CH + tid * VEC, p.top_m, p.vocab_local,
+                      lane, trl);
   }
   // lazy online max: one warp vote per chunk, rarely taken
   const bool up_t = cmt > S.mt + Acc(kSlack);
@@ -522,7 +546,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     }
     const int c = md.chunk;
     if (c == 0) {
-      kind = md.kind;
+      kind = md.kind();
       n = md.n;
       s = n % kSlots;
       const int j = md.item / p.B;
@@ -538,14 +562,20 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       const bool tail = last && (p.vocab_local % CH) != 0;
       Slot<Acc> &sl = sm.slot[s];
       const SlotView sv(sl.area, p.n_chunks * kCW);
-      if (pair)
-        fold_chunk<In, true, NEEDZ>(sm.ring[stage][0], sm.ring[stage][1], tid, c, tail, S, p, warp,
-                                    lane, sl, sv.bmax[0], sv.bmax[1], trl);
-      else
-        fold_chunk<In, false, false>(sm.ring[stage][0], sm.ring[stage][1], tid, c, tail, S, p,
-                                     warp, lane, sl, sv.bmax[0], sv.bmax[1], trl);
+      const uint8_t *sd = sm.ring[stage][0], *st = sm.ring[stage][1];
+      if (pair) {
+        if (!tail)
+          fold_chunk<In, true, NEEDZ, false>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
+                                             sv.bmax[1], trl);
+        else
+          fold_chunk<In, true, NEEDZ, true>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
+                                            sv.bmax[1], trl);
+      } else {
+        fold_chunk<In, false, false, true>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
+                                           sv.bmax[1], trl);
+      }
     } else {
-      sample_chunk<In>(sm.ring[stage][0], sm.ring[stage][1], c, sm.req[md.req].wf,
+      sample_chunk<In>(sm.ring[stage][0], sm.ring[stage][1], c, sm.req[md.req()].wf,
                        reinterpret_cast<double *>(sm.slot[s].area), p, tid, warp, lane);
     }
     TR_ADD(trl, kind == kRegular ? kTrComputeFold : kTrComputeSample, tf);
@@ -599,7 +629,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     if (tid == 0) {
       sl.item = md.item;
       sl.kind = kind;
-      sl.req = md.req;
+      sl.req = md.req();
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.part_full[s]);
@@ -669,14 +699,15 @@ __device__ __noinline__ void merge_partials(const Slot<Acc> &sl, const DevParams
 // overflowed (e.g. rows sorted by id), the listed blocks whose maximum reaches
 // theta_run are re-read. Both fallbacks are exact, only slower.
 template <class In>
-__device__ __noinline__ void select_topm(const Slot<typename InTraits<In>::Acc> &sl, int r,
+__device__ __noinline__ void select_topm(Slot<typename InTraits<In>::Acc> &sl, int r,
                                          const int *bmax, int nblocks, const In *row, int M,
                                          int nlocal, EpiScratch &es, int *sel, int lane,
                                          unsigned long long *trl) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
-  const int th = vload(&sl.ktheta[r]);
+  // the final bins hold every block's lane maxima: the tightest bound
+  const int th = max(vload(&sl.ktheta[r]), theta_from_bins(sl.klist[r], M, lane));
   const int ncap = vload(&sl.ncap[r]);
   TR_ACC(trl, kTrTopmCand, ncap);
   if (ncap <= kCap) {
@@ -1274,9 +1305,8 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
     StageMeta m;
     m.item = item;
     m.chunk = c;
-    m.kind = kind;
     m.n = n;
-    m.req = req;
+    m.kr = kind | (req << 1);
     sm.meta[stage] = m;
     const int rem = nlocal - c * CH;
     const int elems = rem < CH ? rem : CH;
@@ -1351,9 +1381,8 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
   StageMeta m;
   m.item = -1;
   m.chunk = 0;
-  m.kind = kRegular;
   m.n = n;
-  m.req = 0;
+  m.kr = kRegular;
   sm.meta[stage] = m;
   mbar_arrive(&sm.full[stage]);
 }

@@ -20,7 +20,7 @@ names = ["compute_wait_full", "compute_fold", "compute_sample", "compute_wait_sl
          "compute_item_end", "epi_wait_full", "epi_merge", "epi_topm", "epi_decide", "epi_sample",
          "prod_wait_empty", "prod_drain", "prod_items", "prod_samples", "kernel", "epi_items",
          "topm_candidates", "topm_survivors", "topm_fallbacks", "max_survivors", "need_exact",
-         "cap_calls", "compute_cap_lock", "compute_cap"]
+         "cap_calls", "cap_sorts", "compute_cap"]
 B = int(os.environ.get("B", 256))
 V = int(os.environ.get("V", 128256))
 G = int(os.environ.get("G", 8))
@@ -61,7 +61,7 @@ for i, n in enumerate(names):
         res[n] = float(t[:, i].max())
         continue
     if n in ("prod_items", "prod_samples", "epi_items", "kernel", "topm_candidates",
-             "topm_survivors", "topm_fallbacks", "need_exact", "cap_calls"):
+             "topm_survivors", "topm_fallbacks", "need_exact", "cap_calls", "cap_sorts"):
         res[n] = t[:, i].sum() / reps
         continue
     per = {"compute": 16, "epi": 2, "prod": 1}[n.split("_")[0]]
