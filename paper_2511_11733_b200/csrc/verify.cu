@@ -289,8 +289,9 @@ __device__ __forceinline__ Acc key_floor(int th) {
 // Rare path of a block whose maximum reached theta_run (out of line; the
 // stage is still resident, so the values are re-read from shared memory):
 // fold the lane maxima into the bins, raise theta_run when at least M + 2 bins
-// lie above it (one sort), and capture the elements that reach it — only the
-// lanes whose maximum reaches the bound look at their elements.
+// lie above it (a few REDUX.MIN steps, or one sort while the bound is far
+// behind), and capture the elements that reach it — only the lanes whose
+// maximum reaches the bound look at their elements.
 template <class In>
 __device__ __noinline__ void capture_row(Slot<typename InTraits<In>::Acc> &sl, int r, int lkey,
                                          const uint8_t *srow, int id_base, int M, int nlocal,
@@ -306,10 +307,27 @@ __device__ __noinline__ void capture_row(Slot<typename InTraits<In>::Acc> &sl, i
     bin = lkey;  // at least
   }
   int th = vload(&sl.ktheta[r]);
-  if (__popc(__ballot_sync(0xffffffffu, bin > th)) >= M + 2) {
-    TR_INC(trl, kTrCapLock);
+  const int above = __popc(__ballot_sync(0xffffffffu, bin > th));
+  if (above >= M + 2) {
+    // new bound: the M-th largest bin = the k-th smallest of those above th
     __syncwarp();
-    const int nth = theta_from_bins(bins, M, lane);
+    bin = vload(bins + lane);
+    int k = __popc(__ballot_sync(0xffffffffu, bin > th)) - M + 1;
+    int nth = th;
+    if (k <= 8) {
+      // a few REDUX.MIN steps (bins equal to the minimum count with multiplicity)
+      int cur = th;
+      for (;;) {
+        const int m = __reduce_min_sync(0xffffffffu, bin > cur ? bin : INT_MAX);
+        k -= __popc(__ballot_sync(0xffffffffu, bin == m));
+        cur = m;
+        if (k <= 0) break;
+      }
+      nth = cur;
+    } else {
+      TR_INC(trl, kTrCapLock);
+      nth = theta_from_bins(bins, M, lane);
+    }
     if (nth > th) {
       th = nth;
       if (lane == 0) atomicMax(&sl.ktheta[r], nth);
