@@ -168,6 +168,18 @@ dsdv_status dsdv_sample_extra(dsdv_ctx *ctx, const dsdv_params *params,
 dsdv_status dsdv_draft_sample(dsdv_ctx *ctx, const dsdv_params *params,
                               const void *draft_logits, int32_t *draft_tokens, void *stream);
 
+/* Whole-row mixtures of two fp64 probability vectors of length vocab (the
+ * drop-in API's soften and residual_distribution, verifier.cpp:161-186 and
+ * :198-213): DSDV_MIX_SOFTEN w = a^(1-tau) b^tau, DSDV_MIX_RESIDUAL
+ * w = max(0, a - b); out = w / sum(w). *status (device) becomes
+ * DSDV_E_DEGENERATE_MIXTURE / DSDV_E_EMPTY_RESIDUAL when sum(w) <= 0. The
+ * reference's endpoint short-circuits (tau 0 / 1 / equal rows) are the
+ * caller's (they return an input unchanged). */
+enum { DSDV_MIX_SOFTEN = 0, DSDV_MIX_RESIDUAL = 1 };
+dsdv_status dsdv_mix_rows(dsdv_ctx *ctx, int32_t kind, int32_t vocab, const double *a,
+                          const double *b, double tau, double *out, int32_t *status,
+                          void *stream);
+
 /* Waits for `stream`, then reports the first failing sequence's status with a
  * reference-style message in dsdv_last_error (status may be NULL to only sync). */
 dsdv_status dsdv_sync(dsdv_ctx *ctx, const dsdv_params *params, const int32_t *status,

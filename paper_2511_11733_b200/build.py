@@ -25,6 +25,7 @@ LIB_DSDV = PKG / "libdsdv.so"
 LIB_DSD = PKG / "libdsd_b200.so"
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+CUDA_HOME = Path(NVCC).resolve().parent.parent
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
               f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
@@ -83,14 +84,31 @@ def build_dsd_api(force: bool = False) -> Path | None:
     deps = [*srcs, *_headers(), LIB_DSDV]
     if force or _stale(LIB_DSD, deps):
         _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
-              f"-I{INCLUDE}", *map(str, srcs), "-o", str(LIB_DSD),
-              f"-L{PKG}", "-ldsdv", "-Wl,-rpath,$ORIGIN"])
+              f"-I{INCLUDE}", f"-I{CUDA_HOME}/include", *map(str, srcs), "-o", str(LIB_DSD),
+              f"-L{PKG}", "-ldsdv", f"-L{CUDA_HOME}/lib64", "-lcudart", "-Wl,-rpath,$ORIGIN"])
     return LIB_DSD
+
+
+CPP_TESTS = ROOT / "tests" / "cpp"
+
+
+def build_cpp_tests(force: bool = False) -> list[Path]:
+    """C++ test programs of the drop-in API (tests/cpp/*.cpp -> build/cpp/)."""
+    outs = []
+    for src in sorted(CPP_TESTS.glob("*.cpp")):
+        exe = PKG / "bin" / src.stem
+        if force or _stale(exe, [src, *_headers(), LIB_DSD]):
+            exe.parent.mkdir(parents=True, exist_ok=True)
+            _run(["g++", "-std=c++20", "-O2", "-Wall", f"-I{INCLUDE}", str(src), "-o", str(exe),
+                  f"-L{PKG}", "-ldsd_b200", "-ldsdv", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/.."])
+        outs.append(exe)
+    return outs
 
 
 def build_all(force: bool = False) -> None:
     build_dsdv(force)
     build_dsd_api(force)
+    build_cpp_tests(force)
 
 
 if __name__ == "__main__":

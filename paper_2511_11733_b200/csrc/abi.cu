@@ -22,6 +22,8 @@ cudaError_t launch_sample_extra(const DevParams &, const void *, const void *, c
                                 cudaStream_t);
 template <class In>
 cudaError_t launch_draft_sample(const DevParams &, const void *, int32_t *, cudaStream_t);
+cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, double tau,
+                            double *out, int32_t *status, cudaStream_t stream);
 cudaError_t launch_synth(int dtype, int B, int gamma, int V, int stride, uint64_t seed,
                          void *draft, void *target, cudaStream_t stream);
 }  // namespace dsdv
@@ -381,6 +383,22 @@ dsdv_status dsdv_sample_extra(dsdv_ctx *ctx, const dsdv_params *params, const vo
       break;
   }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "sample_extra launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_mix_rows(dsdv_ctx *ctx, int32_t kind, int32_t vocab, const double *a,
+                          const double *b, double tau, double *out, int32_t *status,
+                          void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  if (kind != DSDV_MIX_SOFTEN && kind != DSDV_MIX_RESIDUAL)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_mix_rows: unknown kind %d", kind);
+  if (vocab < 1 || !a || !b || !out || !status)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_mix_rows: bad argument");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  e = dsdv::launch_mix_rows(kind, vocab, a, b, tau, out, status, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "mix_rows launch");
   ctx->launches += 1;
   return DSDV_OK;
 }

@@ -253,6 +253,46 @@ cudaError_t launch_synth(int dtype, int B, int gamma, int V, int stride, uint64_
   return cudaGetLastError();
 }
 
+// Whole-row mixture of two fp64 probability vectors (the drop-in soften,
+// verifier.cpp:161-186, and residual_distribution, :198-213): w_i =
+// a_i^(1-tau) b_i^tau (kind 0) or max(0, a_i - b_i) (kind 1), then w / sum(w)
+// (Distribution::from_weights, distribution.cpp:54-63). One CTA; status is the
+// error the reference throws when the mass is zero.
+__global__ void __launch_bounds__(1024) mix_rows_kernel(int kind, int V, const double *a,
+                                                         const double *b, double tau,
+                                                         double *out, int32_t *status) {
+  __shared__ double part[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const double w = kind == 0 ? pow(a[i], 1.0 - tau) * pow(b[i], tau) : fmax(0.0, a[i] - b[i]);
+    out[i] = w;
+    s += w;
+  }
+  s = warp_sum_f64(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+    t = warp_sum_f64(t);
+    if (threadIdx.x == 0) part[0] = t;
+  }
+  __syncthreads();
+  const double total = part[0];
+  if (!(total > 0.0)) {
+    if (threadIdx.x == 0)
+      *status = kind == 0 ? DSDV_E_DEGENERATE_MIXTURE : DSDV_E_EMPTY_RESIDUAL;
+    return;
+  }
+  for (int i = threadIdx.x; i < V; i += blockDim.x) out[i] /= total;
+  if (threadIdx.x == 0) *status = DSDV_OK;
+}
+
+cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, double tau,
+                            double *out, int32_t *status, cudaStream_t stream) {
+  mix_rows_kernel<<<1, 1024, 0, stream>>>(kind, V, a, b, tau, out, status);
+  return cudaGetLastError();
+}
+
 #define DSDV_INST(T)                                                                             \
   template cudaError_t launch_sample_extra<T>(const DevParams &, const void *, const void *,     \
                                               const double *, const int32_t *, const double *,  \
