@@ -185,6 +185,42 @@ dsdv_status dsdv_mix_rows(dsdv_ctx *ctx, int32_t kind, int32_t vocab, const doub
 dsdv_status dsdv_sync(dsdv_ctx *ctx, const dsdv_params *params, const int32_t *status,
                       void *stream);
 
+/* ---- vocabulary-sharded verification --------
+ * Rank p of P holds ids [vocab_offset, vocab_offset + vocab_local) of every
+ * row (params->vocab = global V; row_stride and pointers refer to the slice).
+ * Per window, with the caller's collectives in between (csrc/shard.cu):
+ *   dsdv_shard_stats   -> all-gather records [P][B][gamma+1][DSDV_RECORD_WORDS]
+ *                         and top lists [P][B][gamma][2][m] (m = min(top_m, V))
+ *   dsdv_shard_merge   (identical on every rank: k, key flags, accept draws)
+ *   dsdv_shard_sample(DSDV_SHARD_MASS)    -> all-gather the [B] masses
+ *   dsdv_shard_sample(DSDV_SHARD_RESOLVE) -> all-reduce(max) the [B] tokens
+ * Decisions equal the unsharded verifier's except inside the eps bands (the
+ * merged fp32 sums are re-associated). */
+dsdv_status dsdv_shard_stats(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,
+                             const void *target_logits, const int32_t *draft_tokens,
+                             double *records, double *top_values, int32_t *top_ids,
+                             void *stream);
+/* out: per-sequence outputs (extra_token is set to -1 until the resolve step),
+ * optional per-position outputs, and out->records (required) receives the
+ * merged global records. position[b] = the row of the extra draw (k for a
+ * residual, gamma for the bonus, -1 when the sequence stopped on an error);
+ * uniform[b] = its Philox draw. */
+dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
+                             const double *records_all, const double *top_values_all,
+                             const int32_t *top_ids_all, const int32_t *draft_tokens,
+                             const dsdv_outputs *out, int32_t *position, double *uniform,
+                             void *stream);
+enum { DSDV_SHARD_MASS = 0, DSDV_SHARD_RESOLVE = 1 };
+/* MASS: mass_out[b] = this slice's weight total of row position[b].
+ * RESOLVE: masses_all = the gathered [nranks][B] totals; token_out[b] = the
+ * global id on the owning rank, -1 elsewhere; status[b] = DSDV_E_EMPTY_RESIDUAL
+ * when the row has no mass. */
+dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t mode, int32_t rank,
+                              int32_t nranks, const void *draft_logits, const void *target_logits,
+                              const double *records, const int32_t *position,
+                              const double *uniform, const double *masses_all, double *mass_out,
+                              int32_t *token_out, int32_t *status, void *stream);
+
 /* ---- helpers ----------------------------------------------------------- */
 /* The accept / extra / draft uniform the kernels use (philox.h), on the host. */
 double dsdv_uniform(uint64_t seed, uint64_t window, uint32_t sequence, uint32_t slot);

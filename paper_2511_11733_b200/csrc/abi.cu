@@ -22,6 +22,15 @@ cudaError_t launch_sample_extra(const DevParams &, const void *, const void *, c
                                 cudaStream_t);
 template <class In>
 cudaError_t launch_draft_sample(const DevParams &, const void *, int32_t *, cudaStream_t);
+cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const double *topv,
+                               const int32_t *topi, int P, const int32_t *tokens, const DevOut &o,
+                               int32_t *position, double *uniform, cudaStream_t stream);
+template <class In>
+cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nranks,
+                                const void *draft, const void *target, const double *records,
+                                const int32_t *position, const double *uniform,
+                                const double *masses, double *mass_out, int32_t *token_out,
+                                int32_t *status, cudaStream_t stream);
 cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, double tau,
                             double *out, int32_t *status, cudaStream_t stream);
 cudaError_t launch_synth(int dtype, int B, int gamma, int V, int stride, uint64_t seed,
@@ -99,7 +108,6 @@ dsdv_status ensure_scratch(dsdv_ctx *ctx, size_t n_positions, size_t n_sequences
   }
   if (n_sequences > ctx->done_cap) {
     if (ctx->done) cudaFree(ctx->done);
-  if (ctx->trace) cudaFree(ctx->trace);
     e = cudaMalloc(&ctx->done, n_sequences * sizeof(unsigned int));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(done)");
     e = cudaMemset(ctx->done, 0, n_sequences * sizeof(unsigned int));
@@ -168,12 +176,17 @@ bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
 dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draft,
                       const void *target, const int32_t *tokens, const dsdv_outputs *out,
-                      void *stream, bool stats_only) {
+                      void *stream, bool stats_only, double *topv = nullptr,
+                      int32_t *topi = nullptr) {
+  const bool partial = topv != nullptr;
   if (!ctx) return DSDV_E_INVARIANT;
   DevParams d;
   dsdv_status st = build_params(ctx, params, d);
   if (st != DSDV_OK) return st;
   d.stats_only = stats_only ? 1 : 0;
+  d.partial = partial ? 1 : 0;
+  if (partial && !topi)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_stats: top lists are required");
   if (!draft || !target || !tokens || !out)
     return fail(ctx, DSDV_E_INVARIANT, "logits, draft tokens and outputs must be non-null");
   if (!aligned16(draft) || !aligned16(target))
@@ -209,7 +222,9 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   }
   s.trace = ctx->trace;
 #endif
-  const DevOut o = to_dev(out);
+  DevOut o = to_dev(out);
+  o.topv = topv;
+  o.topi = topi;
   switch (params->dtype) {
     case DSDV_DTYPE_BF16:
       e = dsdv::launch_fused<__nv_bfloat16>(d, draft, target, tokens, o, s, (cudaStream_t)stream,
@@ -383,6 +398,86 @@ dsdv_status dsdv_sample_extra(dsdv_ctx *ctx, const dsdv_params *params, const vo
       break;
   }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "sample_extra launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_shard_stats(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,
+                             const void *target_logits, const int32_t *draft_tokens,
+                             double *records, double *top_values, int32_t *top_ids,
+                             void *stream) {
+  if (!records || !top_values || !top_ids)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_stats: records and top lists are required");
+  dsdv_outputs out;
+  std::memset(&out, 0, sizeof(out));
+  out.records = records;
+  return run_fused(ctx, params, draft_logits, target_logits, draft_tokens, &out, stream, true,
+                   top_values, top_ids);
+}
+
+dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
+                             const double *records_all, const double *top_values_all,
+                             const int32_t *top_ids_all, const int32_t *draft_tokens,
+                             const dsdv_outputs *out, int32_t *position, double *uniform,
+                             void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  DevParams d;
+  dsdv_status st = build_params(ctx, params, d);
+  if (st != DSDV_OK) return st;
+  if (!records_all || !top_values_all || !top_ids_all || !draft_tokens || !out || !position ||
+      !uniform || !out->records || !out->accepted_count || !out->extra_token ||
+      !out->extra_source || !out->key_count || !out->status || !out->near_threshold)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_merge: null argument");
+  if (nranks < 1 || nranks > 64)
+    return fail(ctx, DSDV_E_UNSUPPORTED, "dsdv_shard_merge: 1..64 ranks, got %d", nranks);
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  const DevOut o = to_dev(out);
+  e = dsdv::launch_shard_merge(d, records_all, top_values_all, top_ids_all, nranks, draft_tokens,
+                               o, position, uniform, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "shard_merge launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t mode, int32_t rank,
+                              int32_t nranks, const void *draft_logits, const void *target_logits,
+                              const double *records, const int32_t *position,
+                              const double *uniform, const double *masses_all, double *mass_out,
+                              int32_t *token_out, int32_t *status, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  DevParams d;
+  dsdv_status st = build_params(ctx, params, d);
+  if (st != DSDV_OK) return st;
+  if (mode != DSDV_SHARD_MASS && mode != DSDV_SHARD_RESOLVE)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_sample: unknown mode %d", mode);
+  if (!draft_logits || !target_logits || !records || !position || !uniform ||
+      (mode == DSDV_SHARD_MASS && !mass_out) ||
+      (mode == DSDV_SHARD_RESOLVE && (!masses_all || !token_out || !status)))
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_sample: null argument");
+  if (rank < 0 || rank >= nranks)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_sample: rank %d of %d", rank, nranks);
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  switch (params->dtype) {
+    case DSDV_DTYPE_BF16:
+      e = dsdv::launch_shard_sample<__nv_bfloat16>(d, mode, rank, nranks, draft_logits,
+                                                   target_logits, records, position, uniform,
+                                                   masses_all, mass_out, token_out, status,
+                                                   (cudaStream_t)stream);
+      break;
+    case DSDV_DTYPE_F32:
+      e = dsdv::launch_shard_sample<float>(d, mode, rank, nranks, draft_logits, target_logits,
+                                           records, position, uniform, masses_all, mass_out,
+                                           token_out, status, (cudaStream_t)stream);
+      break;
+    default:
+      e = dsdv::launch_shard_sample<double>(d, mode, rank, nranks, draft_logits, target_logits,
+                                            records, position, uniform, masses_all, mass_out,
+                                            token_out, status, (cudaStream_t)stream);
+      break;
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "shard_sample launch");
   ctx->launches += 1;
   return DSDV_OK;
 }

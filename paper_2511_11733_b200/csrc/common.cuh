@@ -44,6 +44,7 @@ struct DevParams {
   int n_chunks;     // chunks per row
   int n_items;      // B * (gamma + 1)
   int stats_only;   // 1: dsdv_window_stats (no draws, no waits, no sampling)
+  int partial;      // 1: dsdv_shard_stats (partial records of a vocabulary slice only)
   int need_z;       // 0 < tau < 1
   float tau_f, omt_f;
   double tau, ratio_limit, gap_limit, overlap_floor, eps_u, eps_lambda;
@@ -57,6 +58,8 @@ struct DevOut {
   uint8_t *extra_source, *key_mask, *accepted;
   double *accept_prob, *h_target, *h_draft, *p_target_y, *p_draft_y, *norm_match,
       *p_effective_y, *uniform, *records;
+  double *topv;    // sharded partial: [B][gamma][2][M] top-m values (target, draft)
+  int32_t *topi;   //                  and global ids
 };
 
 struct DevScratch {

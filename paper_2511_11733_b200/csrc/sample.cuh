@@ -124,11 +124,12 @@ __device__ __forceinline__ void vec_weights(const uint4 &rt, const uint4 &rd, in
 }
 
 // Called by all kConsumerThreads threads (thread index `tid` in [0, 256)).
-// Returns the sampled local index, or -1 when the weights have no mass.
+// Returns the sampled local index, or -1 when the weights have no mass; the
+// total weight stays in sh->W until the next call.
 template <class In, class Acc>
 __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const Weigher<Acc> &wf_s,
                                        int n, double u, double eps, SampleShared *sh, int tid,
-                                       int *near_out) {
+                                       int *near_out, double t_override = -1.0) {
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int U = 4;  // tiles in flight per warp
   const Weigher<Acc> wf = wf_s;
@@ -197,7 +198,9 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
       W += sh->warp_total[w];
       L = max(L, sh->warp_last[w]);
     }
-    const double T = u * W;
+    // t_override >= 0: the boundary was placed by the caller (a vocabulary
+    // slice of a sharded row, T relative to this slice's first id)
+    const double T = t_override >= 0.0 ? t_override : u * W;
     double run = 0.0;
     int found = -1;
     double base = 0.0;

@@ -174,7 +174,8 @@ struct EpiScratch {
   int cand[32];          // candidate blocks of one 32-block batch
   int ev_id[128];        // surviving elements (id, value)
   double ev_key[128];
-  int sel[2][kMaxTopM];  // top-m ids of the target / draft row
+  int sel[2][kMaxTopM];     // top-m ids of the target / draft row
+  double selv[2][kMaxTopM];  // and their values (sharded partial records)
 };
 
 template <class Acc>
@@ -719,11 +720,17 @@ __device__ __noinline__ void merge_partials(const Slot<Acc> &sl, const DevParams
 template <class In>
 __device__ __noinline__ void select_topm(Slot<typename InTraits<In>::Acc> &sl, int r,
                                          const int *bmax, int nblocks, const In *row, int M,
-                                         int nlocal, EpiScratch &es, int *sel, int lane,
-                                         unsigned long long *trl) {
+                                         int nlocal, EpiScratch &es, int *sel, double *selv,
+                                         int lane, unsigned long long *trl) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
+  // a vocabulary slice shorter than M leaves (-1, -inf) entries
+  if (lane < M) {
+    sel[lane] = -1;
+    selv[lane] = -INFINITY;
+  }
+  __syncwarp();
   // the final bins hold every block's lane maxima: the tightest bound
   const int th = max(vload(&sl.ktheta[r]), theta_from_bins(sl.klist[r], M, lane));
   const int ncap = vload(&sl.ncap[r]);
@@ -762,7 +769,10 @@ __device__ __noinline__ void select_topm(Slot<typename InTraits<In>::Acc> &sl, i
           const double vk = es.ev_key[k];
           rank += (vk > vi || (vk == vi && es.ev_id[k] < ii)) ? 1 : 0;
         }
-        if (rank < M) sel[rank] = ii;
+        if (rank < M) {
+          sel[rank] = ii;
+          selv[rank] = vi;
+        }
       }
       __syncwarp();
       return;
@@ -783,7 +793,10 @@ __device__ __noinline__ void select_topm(Slot<typename InTraits<In>::Acc> &sl, i
         if (cv >= L.theta) L.insert(cv, ci, M, lane);
       }
     }
-    if (lane < M) sel[lane] = L.id;
+    if (lane < M && L.id != 0x7fffffff) {
+      sel[lane] = L.id;
+      selv[lane] = (double)L.v;
+    }
     __syncwarp();
     return;
   }
@@ -820,7 +833,10 @@ __device__ __noinline__ void select_topm(Slot<typename InTraits<In>::Acc> &sl, i
       }
     }
   }
-  if (lane < M) sel[lane] = L.id;
+  if (lane < M && L.id != 0x7fffffff) {
+    sel[lane] = L.id;
+    selv[lane] = (double)L.v;
+  }
   __syncwarp();
 }
 
@@ -1115,6 +1131,65 @@ __device__ __noinline__ int resolve_tile(const In *rt, const In *rd,
   return idx;
 }
 
+// Sharded verifier (dsdv_shard_stats): the partial record of one position over
+// this vocabulary slice, merged across slices by shard.cu (log-sum-exp of the
+// per-slice normalisers, P-way merge of the top-m lists). Record words:
+//   [0] m_t  [1] ln s_t  [2] m_d  [3] ln s_d  [4] ln s_z (relative to
+//   (1-tau) m_t + tau m_d; -inf when the slice holds no mix mass)
+//   [5] l_t(y) [6] l_d(y) (NaN unless y lies in this slice)
+//   [7] rows differ | y in slice << 1
+// and the slice's top-M (value, global id) of each row, (value desc, id asc).
+template <class In>
+__device__ __noinline__ void write_partial(const DevOut &o, const DevParams &p, int b, int j,
+                                           bool pair, const double (&mrg)[7], int diff,
+                                           const EpiScratch &es, const In *rt, const In *rd,
+                                           const int32_t *tokens, int lane) {
+  using Acc = typename InTraits<In>::Acc;
+  const double Mt = mrg[0], St = mrg[1], Md = mrg[2], Sd = mrg[3], Sz = mrg[4];
+  const double MtL = mrg[5], MdL = mrg[6];
+  const double dd = (double)log2e<Acc>() * kLn2 - 1.0;
+  const double omt = (double)p.omt_f, tau = (double)p.tau_f;
+  double lsz = 0.0;
+  if (pair && p.need_z) {
+    if (Sz > 1e-30 && isfinite(Sz)) {
+      const double zL = omt * MtL + tau * MdL, z = omt * Mt + tau * Md;
+      lsz = (zL + log2(Sz)) * kLn2 - dd * z - z;
+    } else {
+      lsz = exact_lse_mix_warp<In>(rt, rd, p.vocab_local, omt, tau, lane) - (omt * Mt + tau * Md);
+    }
+  }
+  const int G1 = p.gamma + 1;
+  if (lane == 0) {
+    double *r = o.records + ((size_t)b * G1 + j) * kRecordWords;
+    r[0] = Mt;
+    r[1] = (MtL + log2(St)) * kLn2 - dd * Mt - Mt;
+    if (pair) {
+      const int y = tokens[(size_t)b * p.gamma + j];
+      const int yl = y - p.vocab_offset;
+      const bool own = yl >= 0 && yl < p.vocab_local;
+      r[2] = Md;
+      r[3] = (MdL + log2(Sd)) * kLn2 - dd * Md - Md;
+      r[4] = lsz;
+      r[5] = own ? load_scalar<In>(rt + yl) : NAN;
+      r[6] = own ? load_scalar<In>(rd + yl) : NAN;
+      r[7] = (double)((diff ? 1 : 0) | (own ? 2 : 0));
+    } else {
+      r[2] = r[3] = r[4] = 0.0;
+      r[5] = r[6] = NAN;
+      r[7] = 0.0;
+    }
+  }
+  const int M = p.top_m;
+  if (pair && lane < M) {
+    const size_t base = ((size_t)b * p.gamma + j) * 2 * M;
+    const int it = es.sel[0][lane], id = es.sel[1][lane];
+    o.topv[base + lane] = es.selv[0][lane];
+    o.topi[base + lane] = it >= 0 ? p.vocab_offset + it : -1;
+    o.topv[base + M + lane] = es.selv[1][lane];
+    o.topi[base + M + lane] = id >= 0 ? p.vocab_offset + id : -1;
+  }
+}
+
 template <class In>
 __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
                               const In *__restrict__ draft, const In *__restrict__ target,
@@ -1152,8 +1227,10 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
         EpiScratch &es = sm.epi[ew];
         const int nb = p.n_chunks * kCW;
         const SlotView sv(sl.area, nb);
-        select_topm<In>(sl, 0, sv.bmax[0], nb, rt, M, p.vocab_local, es, es.sel[0], lane, trl);
-        select_topm<In>(sl, 1, sv.bmax[1], nb, rd, M, p.vocab_local, es, es.sel[1], lane, trl);
+        select_topm<In>(sl, 0, sv.bmax[0], nb, rt, M, p.vocab_local, es, es.sel[0], es.selv[0],
+                        lane, trl);
+        select_topm<In>(sl, 1, sv.bmax[1], nb, rd, M, p.vocab_local, es, es.sel[1], es.selv[1],
+                        lane, trl);
         reset_capture(sl, lane);
         const int did = lane < M ? es.sel[1][lane] : -1;
         bool found = false;
@@ -1165,7 +1242,11 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       TR_ADD(trl, kTrEpiTopm, tt);
       TR_START(td);
       TR_INC(trl, kTrEpiItems);
-
+      if (p.partial) {
+        // vocabulary-sharded verifier: this slice's partial record only
+        const EpiScratch &es = sm.epi[ew];
+        write_partial<In>(o, p, b, j, pair, mrg, diff, es, rt, rd, tokens, lane);
+      } else {
       PosEval ev;
       if (lane == 0) {
         const int y = pair ? tokens[(size_t)b * p.gamma + j] : 0;
@@ -1240,6 +1321,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
           }
         }
       }
+      }  // !p.partial
       TR_ADD(trl, kTrEpiDecide, td);
     } else {
       // ---- sample item: scan the tile sums for T = u W, resolve the tile ----

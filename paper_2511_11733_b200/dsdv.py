@@ -82,6 +82,12 @@ def _load() -> C.CDLL:
         "dsdv_uniform": (C.c_double, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]),
         "dsdv_synth_logits": (st, [vp, C.POINTER(_Params), C.c_uint64, vp, vp, vp]),
         "dsdv_launch_count": (C.c_uint64, [vp]),
+        "dsdv_shard_stats": (st, [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp]),
+        "dsdv_shard_merge": (st, [vp, C.POINTER(_Params), C.c_int32, vp, vp, vp, vp,
+                                  C.POINTER(_Outputs), vp, vp, vp]),
+        "dsdv_shard_sample": (st, [vp, C.POINTER(_Params), C.c_int32, C.c_int32, C.c_int32, vp,
+                                   vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "dsdv_mix_rows": (st, [vp, C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -93,7 +99,8 @@ def _load() -> C.CDLL:
 LIB = _load()
 EXPORTED = ("dsdv_create", "dsdv_destroy", "dsdv_last_error", "dsdv_abi_version", "dsdv_validate",
             "dsdv_verify", "dsdv_window_stats", "dsdv_sample_extra", "dsdv_draft_sample",
-            "dsdv_sync", "dsdv_uniform", "dsdv_synth_logits", "dsdv_launch_count")
+            "dsdv_sync", "dsdv_uniform", "dsdv_synth_logits", "dsdv_launch_count",
+            "dsdv_shard_stats", "dsdv_shard_merge", "dsdv_shard_sample", "dsdv_mix_rows")
 
 
 def uniform(seed: int, window: int, sequence: int, slot: int) -> float:
