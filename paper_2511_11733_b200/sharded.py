@@ -50,9 +50,11 @@ class TorchComm:
         self.size = dist.get_world_size(group)
 
     def all_gather(self, t: torch.Tensor) -> torch.Tensor:
-        out = torch.empty((self.size, *t.shape), dtype=t.dtype, device=t.device)
-        self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
-        return out
+        """[size, *t.shape]: every rank's tensor in rank (= shard) order."""
+        flat = t.contiguous().reshape(-1)
+        out = torch.empty(self.size * flat.numel(), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, flat, group=self.group)
+        return out.view(self.size, *t.shape)
 
     def all_reduce_max(self, t: torch.Tensor) -> torch.Tensor:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)

@@ -47,13 +47,3 @@ def test_sharded_equals_unsharded_gpu(verifier, oracle):
     same = float((gpu["accepted_count"] == uns["accepted_count"]).float().mean())
     assert same >= 0.95
     assert bool((gpu["norm_match"] == uns["norm_match"]).all())
-
-
-def test_slice_bounds_cover_the_vocabulary():
-    for V in (128256, 151936, 32000, 1000):
-        for P in (2, 3, 4, 8):
-            parts = [slice_bounds(V, P, r) for r in range(P)]
-            assert parts[0][0] == 0
-            assert sum(n for _, n in parts) == V
-            for (lo, n), (lo2, _) in zip(parts, parts[1:]):
-                assert lo + n == lo2 and lo2 % 8 == 0
