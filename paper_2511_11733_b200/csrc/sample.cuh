@@ -45,6 +45,9 @@ struct Weigher {
   Acc md, cd_hi, cd_lo;  // P_d(i)  = exp((d_i - md) - cd)
   Acc omt, tau;          // softened: exp(omt (t_i - mt) + tau (d_i - md) - cz)
   Acc cz_hi, cz_lo;
+  // fp32 packed path (weigh_vec): exponents in log2 units, constants split
+  // hi/lo so that they stay exact relative to the (small) exponent
+  float kt_hi, kt_lo, kd_hi, kd_lo, kz_hi, kz_lo, omtL, tauL;
 
   __device__ __forceinline__ Acc p_t(Acc t) const {
     return fast_exp2(mul_rn(sub_rn(sub_rn(sub_rn(t, mt), ct_hi), ct_lo), log2e<Acc>()));
@@ -63,6 +66,49 @@ struct Weigher {
     return w > Acc(0) ? w : Acc(0);
   }
 };
+
+// Weights of one 16-byte vector of each row. fp32: packed f32x2 arithmetic,
+// one FFMA2 + FADD2 per exponent pair (a = t - mt is exact for bf16 / fp32
+// rows near the maximum); every call site (streaming pass, crossing-tile
+// re-read) evaluates the identical instruction sequence, so tile sums and the
+// resolve agree bit for bit. fp64: the scalar correctly rounded form.
+template <int VEC>
+__device__ __forceinline__ void weigh_vec(const Weigher<float> &wf, const float (&vt)[VEC],
+                                          const float (&vd)[VEC], float (&w)[VEC]) {
+  const f32x2 L2 = pk2(kLog2eF, kLog2eF);
+  const f32x2 mt2 = pk2(wf.mt, wf.mt), kth = pk2(wf.kt_hi, wf.kt_hi), ktl = pk2(wf.kt_lo, wf.kt_lo);
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    const f32x2 a2 = sub2(pk2(vt[e], vt[e + 1]), mt2);
+    f32x2 r;
+    if (wf.kind == kWeightPlain) {
+      const f32x2 xt = add2(fma2(a2, L2, kth), ktl);
+      r = pk2(fast_exp2(lo2(xt)), fast_exp2(hi2(xt)));
+    } else {
+      const f32x2 b2 = sub2(pk2(vd[e], vd[e + 1]), pk2(wf.md, wf.md));
+      const f32x2 xd = add2(fma2(b2, L2, pk2(wf.kd_hi, wf.kd_hi)), pk2(wf.kd_lo, wf.kd_lo));
+      const f32x2 pd = pk2(fast_exp2(lo2(xd)), fast_exp2(hi2(xd)));
+      f32x2 xe;
+      if (wf.kind == kWeightResTarget)
+        xe = add2(fma2(a2, L2, kth), ktl);
+      else
+        xe = add2(fma2(pk2(wf.omtL, wf.omtL), a2,
+                       fma2(pk2(wf.tauL, wf.tauL), b2, pk2(wf.kz_hi, wf.kz_hi))),
+                  pk2(wf.kz_lo, wf.kz_lo));
+      const f32x2 pe = pk2(fast_exp2(lo2(xe)), fast_exp2(hi2(xe)));
+      r = sub2(pe, pd);
+      r = pk2(fmaxf(lo2(r), 0.f), fmaxf(hi2(r), 0.f));
+    }
+    w[e] = lo2(r);
+    w[e + 1] = hi2(r);
+  }
+}
+template <int VEC>
+__device__ __forceinline__ void weigh_vec(const Weigher<double> &wf, const double (&vt)[VEC],
+                                          const double (&vd)[VEC], double (&w)[VEC]) {
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) w[e] = wf(vt[e], vd[e]);
+}
 
 template <class Acc>
 __device__ __forceinline__ void split_hi_lo(double c, Acc &hi, Acc &lo) {
@@ -91,6 +137,12 @@ __device__ __forceinline__ void set_weigher(Weigher<Acc> &wf, int kind, const Po
   // LSE_z relative to the rounded reference points
   const double lz = omt * (ev.mt - (double)wf.mt) + tau * (ev.md - (double)wf.md) + ev.lsz;
   split_hi_lo(lz, wf.cz_hi, wf.cz_lo);
+  // packed fp32 constants (log2 units, relative to the rounded maxima)
+  split_hi_lo(-(ev.lst + (ev.mt - (double)wf.mt)) * kLog2e, wf.kt_hi, wf.kt_lo);
+  split_hi_lo(-(ev.lsd + (ev.md - (double)wf.md)) * kLog2e, wf.kd_hi, wf.kd_lo);
+  split_hi_lo(-lz * kLog2e, wf.kz_hi, wf.kz_lo);
+  wf.omtL = (float)(omt * kLog2e);
+  wf.tauL = (float)(tau * kLog2e);
 }
 
 constexpr int kMaxTiles = 512;
@@ -119,8 +171,10 @@ __device__ __forceinline__ void vec_weights(const uint4 &rt, const uint4 &rd, in
   Acc vt[VEC], vd[VEC];
   unpack(rt, vt, (In *)nullptr);
   unpack(rd, vd, (In *)nullptr);
+  weigh_vec<VEC>(wf, vt, vd, w);
 #pragma unroll
-  for (int e = 0; e < VEC; ++e) w[e] = (base + e < n) ? wf(vt[e], vd[e]) : Acc(0);
+  for (int e = 0; e < VEC; ++e)
+    if (base + e >= n) w[e] = Acc(0);
 }
 
 // Called by all kConsumerThreads threads (thread index `tid` in [0, 256)).

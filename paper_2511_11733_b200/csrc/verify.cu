@@ -521,12 +521,11 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
 #pragma unroll
       for (int e = 0; e < VEC; ++e) vd[e] = Acc(0);
     }
+    Acc w[VEC];
+    weigh_vec<VEC>(wf, vt, vd, w);
     Acc ls = Acc(0);
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      const Acc w = (id0 + e < p.vocab_local) ? wf(vt[e], vd[e]) : Acc(0);
-      ls = add_rn(ls, w);
-    }
+    for (int e = 0; e < VEC; ++e) ls = add_rn(ls, (id0 + e < p.vocab_local) ? w[e] : Acc(0));
     const double ts = warp_sum_f64((double)ls);
     if (lane == 0) tiles[(chunk * kVecs + h) * kCW + warp] = ts;
   }
@@ -1062,10 +1061,15 @@ __device__ __noinline__ int resolve_tile(const In *rt, const In *rd,
       for (int e = 0; e < VEC; ++e) vd[e] = Acc(0);
     }
   }
+  if (!ok) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) vt[e] = vd[e] = Acc(0);
+  }
+  weigh_vec<VEC>(wf, vt, vd, wt);
   double ls = 0.0;
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {
-    wt[e] = (ok && id0 + e < p.vocab_local) ? wf(vt[e], vd[e]) : Acc(0);
+    if (!(ok && id0 + e < p.vocab_local)) wt[e] = Acc(0);
     ls += (double)wt[e];
   }
   int result = -1;
