@@ -114,6 +114,13 @@ __device__ __forceinline__ void unpack(const uint4 &r, double (&v)[2], double *)
   v[1] = __hiloint2double((int)r.w, (int)r.z);
 }
 
+// One element from shared memory (the resident ring stage).
+__device__ __forceinline__ float load_smem_scalar(const __nv_bfloat16 *p) {
+  return __bfloat162float(*p);
+}
+__device__ __forceinline__ float load_smem_scalar(const float *p) { return *p; }
+__device__ __forceinline__ double load_smem_scalar(const double *p) { return *p; }
+
 template <class In>
 __device__ __forceinline__ double load_scalar(const In *p);
 template <>
@@ -255,6 +262,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "r"(a), "r"(parity), "r"(0x989680u)
         : "memory");
   } while (!done);
+}
+// One probe of an mbarrier phase (no suspend): true once the phase completed.
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+      "p; }"
+      : "=r"(done)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
 }
 // 1-D bulk copy global -> shared (TMA engine), completion on an mbarrier.
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,

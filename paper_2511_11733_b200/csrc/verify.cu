@@ -46,14 +46,20 @@
 namespace dsdv {
 namespace fz {
 
-constexpr int kCW = 16;              // compute warps
+#ifndef DSDV_KCW
+#define DSDV_KCW 16
+#endif
+constexpr int kCW = DSDV_KCW;        // compute warps
 constexpr int kCT = kCW * 32;        // compute threads
 constexpr int kEW = 2;               // epilogue warps (alternate stream items)
 constexpr int kEpiWarp = kCW;        // first epilogue warp index
 constexpr int kProdWarp = kCW + kEW; // producer warp index
 constexpr int kThreads = (kCW + kEW + 1) * 32;
-constexpr int kRowBytes = 16384;     // per row per ring stage
-constexpr int kVecs = kRowBytes / 16 / kCT;  // 16-byte vectors per compute thread per row (4)
+#ifndef DSDV_KVECS
+#define DSDV_KVECS 2
+#endif
+constexpr int kVecs = DSDV_KVECS;    // 16-byte vectors per compute thread per row and stage
+constexpr int kRowBytes = kCT * 16 * kVecs;  // per row per ring stage (16 KB)
 constexpr int kSlots = 4;
 // ring depth: 4 x 32 KB stages (3 for fp64 rows, whose slots are larger)
 template <class Acc>
@@ -281,54 +287,50 @@ __device__ __noinline__ int theta_from_bins(const int *bins, int M, int lane) {
   return __shfl_sync(0xffffffffu, sorted, M - 1);
 }
 
+// Epilogue warp, while it waits for a slot: re-derive theta_run of both rows
+// of the item being folded into it (the bins only grow, so any value derived
+// from them stays a valid bound).
+template <class Acc>
+__device__ __noinline__ void refresh_theta(Slot<Acc> &sl, int M, int lane) {
+#pragma unroll 1
+  for (int r = 0; r < 2; ++r) {
+    const int th = vload(&sl.ktheta[r]);
+    const int bin = vload(&sl.klist[r][lane]);
+    if (__popc(__ballot_sync(0xffffffffu, bin > th)) >= M + 1) {
+      const int sorted = warp_sort_desc(bin, lane);
+      const int nth = __shfl_sync(0xffffffffu, sorted, M - 1);
+      if (lane == 0 && nth > th) atomicMax(&sl.ktheta[r], nth);
+    }
+  }
+}
+
 // key(v) >= th  <=>  v >= fkey_inv(th) (keys round toward -inf)
 template <class Acc>
 __device__ __forceinline__ Acc key_floor(int th) {
   return th == INT_MIN ? neg_inf<Acc>() : (Acc)fkey_inv(th);
 }
 
-// Rare path of a block whose maximum reached theta_run (out of line; the
-// stage is still resident, so the values are re-read from shared memory):
-// fold the lane maxima into the bins, raise theta_run when at least M + 2 bins
-// lie above it (a few REDUX.MIN steps, or one sort while the bound is far
-// behind), and capture the elements that reach it — only the lanes whose
-// maximum reaches the bound look at their elements.
-template <class In>
-__device__ __noinline__ void capture_row(Slot<typename InTraits<In>::Acc> &sl, int r, int lkey,
-                                         const uint8_t *srow, int id_base, int M, int nlocal,
-                                         int lane, unsigned long long *trl) {
-  using Acc = typename InTraits<In>::Acc;
-  constexpr int VEC = InTraits<In>::kVec;
-  TR_START(tc);
+// Rare path of a block whose maximum reached theta_run (inline; the values
+// are still in registers): fold the lane maxima into the bins, raise
+// theta_run while it is far behind (one sort, out of line; small raises are
+// left to the epilogue warps, refresh_theta), and capture the elements that
+// reach it. Only lanes whose maximum reaches the bound enter the capture, and
+// each captured element is re-read from the resident stage by its index, so
+// the divergent part costs a few instructions per captured element.
+template <class In, bool TAIL, class Acc, int VEC>
+__device__ __forceinline__ void capture_row(Slot<Acc> &sl, int r, int lkey, int th,
+                                            const Acc (&v)[kVecs][VEC], const uint8_t *srow,
+                                            int c, int tid, int lane, const DevParams &p,
+                                            unsigned long long *trl) {
+  constexpr int CH = kRowBytes / (int)sizeof(In);
   TR_INC(trl, kTrCapCalls);
   int *bins = sl.klist[r];
-  int bin = vload(bins + lane);
-  if (lkey > bin) {
-    atomicMax(bins + lane, lkey);
-    bin = lkey;  // at least
-  }
-  int th = vload(&sl.ktheta[r]);
-  const int above = __popc(__ballot_sync(0xffffffffu, bin > th));
-  if (above >= M + 2) {
-    // new bound: the M-th largest bin = the k-th smallest of those above th
+  const int bin = vload(bins + lane);
+  if (lkey > bin) atomicMax(bins + lane, lkey);
+  if (__popc(__ballot_sync(0xffffffffu, max(bin, lkey) > th)) >= p.top_m + 8) {
+    TR_INC(trl, kTrCapLock);
     __syncwarp();
-    bin = vload(bins + lane);
-    int k = __popc(__ballot_sync(0xffffffffu, bin > th)) - M + 1;
-    int nth = th;
-    if (k <= 8) {
-      // a few REDUX.MIN steps (bins equal to the minimum count with multiplicity)
-      int cur = th;
-      for (;;) {
-        const int m = __reduce_min_sync(0xffffffffu, bin > cur ? bin : INT_MAX);
-        k -= __popc(__ballot_sync(0xffffffffu, bin == m));
-        cur = m;
-        if (k <= 0) break;
-      }
-      nth = cur;
-    } else {
-      TR_INC(trl, kTrCapLock);
-      nth = theta_from_bins(bins, M, lane);
-    }
+    const int nth = theta_from_bins(bins, p.top_m, lane);
     if (nth > th) {
       th = nth;
       if (lane == 0) atomicMax(&sl.ktheta[r], nth);
@@ -336,24 +338,27 @@ __device__ __noinline__ void capture_row(Slot<typename InTraits<In>::Acc> &sl, i
   }
   if (lkey >= th) {
     const Acc thv = key_floor<Acc>(th);
-#pragma unroll 1
-    for (int h = 0; h < kVecs; ++h) {
-      const int q = h * kCT;  // + tid folded into srow / id_base
-      Acc v[VEC];
-      unpack(lds128(srow + q * 16), v, (In *)nullptr);
-      const int id0 = id_base + q * VEC;
+    unsigned keep = 0;
 #pragma unroll
-      for (int e = 0; e < VEC; ++e)
-        if (v[e] >= thv && id0 + e < nlocal) {
-          const int at = atomicAdd(&sl.ncap[r], 1);
-          if (at < kCap) {
-            sl.cap_id[r][at] = id0 + e;
-            sl.cap_v[r][at] = v[e];
-          }
-        }
+    for (int h = 0; h < kVecs; ++h)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const bool ok = !TAIL || c * CH + (h * kCT + tid) * VEC + e < p.vocab_local;
+        keep |= (ok && v[h][e] >= thv ? 1u : 0u) << (h * VEC + e);
+      }
+    int at = atomicAdd(&sl.ncap[r], __popc(keep));
+    while (keep) {
+      const int bit = __ffs(keep) - 1;
+      keep &= keep - 1;
+      const int q = (bit / VEC) * kCT + tid, e = bit % VEC;
+      const In *src = reinterpret_cast<const In *>(srow + q * 16) + e;
+      if (at < kCap) {
+        sl.cap_id[r][at] = c * CH + q * VEC + e;
+        sl.cap_v[r][at] = (Acc)load_smem_scalar(src);
+      }
+      ++at;
     }
   }
-  TR_ADD(trl, kTrCapCycles, tc);
 }
 
 template <bool PAIR, bool NEEDZ, int VEC>
@@ -471,13 +476,11 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
       bmax_t[c * kCW + warp] = bt;
       bmax_d[c * kCW + warp] = bd;
     }
-    // this thread's first vector: byte tid*16 of the stage, id c*CH + tid*VEC
-    if (bt >= vload(&sl.ktheta[0]))
-      capture_row<In>(sl, 0, lt, starget + tid * 16, c * CH + tid * VEC, p.top_m, p.vocab_local,
-                      lane, trl);
-    if (bd >= vload(&sl.ktheta[1]))
-      capture_row<In>(sl, 1, ld, sdraft + tid * 16, c * CH + tid * VEC, p.top_m, p.vocab_local,
-                      lane, trl);
+    const int th0 = vload(&sl.ktheta[0]), th1 = vload(&sl.ktheta[1]);
+    if (bt >= th0 || bd >= th1) {
+      if (bt >= th0) capture_row<In, TAIL>(sl, 0, lt, th0, vt, starget, c, tid, lane, p, trl);
+      if (bd >= th1) capture_row<In, TAIL>(sl, 1, ld, th1, vd, sdraft, c, tid, lane, p, trl);
+    }
   }
   // lazy online max: one warp vote per chunk, rarely taken
   const bool up_t = cmt > S.mt + Acc(kSlack);
@@ -1208,7 +1211,11 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
   for (int n = ew;; n += kEW) {
     const int si = n % kSlots;
     TR_START(tw);
-    mbar_wait(&sm.part_full[si], (n / kSlots) & 1);
+    // while the compute warps fold this slot's item, keep its top-m bound tight
+    while (!mbar_test(&sm.part_full[si], (n / kSlots) & 1)) {
+      refresh_theta(sm.slot[si], M, lane);
+      __nanosleep(64);
+    }
     TR_ADD(trl, kTrEpiWaitFull, tw);
     TR_START(tx);
     Slot<Acc> &sl = sm.slot[si];
