@@ -60,14 +60,20 @@ constexpr int kThreads = (kCW + kEW + 1) * 32;
 #endif
 constexpr int kVecs = DSDV_KVECS;    // 16-byte vectors per compute thread per row and stage
 constexpr int kRowBytes = kCT * 16 * kVecs;  // per row per ring stage (16 KB)
+// 16-byte vector h (< kVecs) of (warp, lane) inside a row chunk: each warp owns
+// kVecs * 32 consecutive vectors, so a (chunk, warp) block is a contiguous id
+// range (block maxima, sample tiles), and each LDS.128 is conflict-free.
+__device__ __forceinline__ int vec_index(int h, int warp, int lane) {
+  return (warp * kVecs + h) * 32 + lane;
+}
 constexpr int kSlots = 4;
 // ring depth: 4 x 32 KB stages (3 for fp64 rows, whose slots are larger)
 template <class Acc>
 struct Ring {
-  static constexpr int kStages = sizeof(Acc) == 8 ? 3 : 4;
+  static constexpr int kStages = sizeof(Acc) == 8 ? 4 : 5;
 };
-constexpr int kMaxTiles = 2048;      // blocks per slot: (chunk, vector, warp), 32*VEC ids each
-constexpr int kAreaBytes = 16384;    // per-slot block maxima, or sample tiles
+constexpr int kMaxTiles = 1024;      // blocks per slot: (chunk, warp), kVecs*32*VEC ids each
+constexpr int kAreaBytes = 8 * kMaxTiles;  // per-slot block maxima (2 x int), or sample tiles (double)
 constexpr int kCap = 256;            // captured top-m candidates per row and item
 constexpr int kReq = 16;             // sample-request queue
 constexpr float kSlack = 8.0f;       // lazy max: rescale when a value exceeds m by this much
@@ -343,14 +349,14 @@ __device__ __forceinline__ void capture_row(Slot<Acc> &sl, int r, int lkey, int 
     for (int h = 0; h < kVecs; ++h)
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        const bool ok = !TAIL || c * CH + (h * kCT + tid) * VEC + e < p.vocab_local;
+        const bool ok = !TAIL || c * CH + vec_index(h, tid >> 5, lane) * VEC + e < p.vocab_local;
         keep |= (ok && v[h][e] >= thv ? 1u : 0u) << (h * VEC + e);
       }
     int at = atomicAdd(&sl.ncap[r], __popc(keep));
     while (keep) {
       const int bit = __ffs(keep) - 1;
       keep &= keep - 1;
-      const int q = (bit / VEC) * kCT + tid, e = bit % VEC;
+      const int q = vec_index(bit / VEC, tid >> 5, lane), e = bit % VEC;
       const In *src = reinterpret_cast<const In *>(srow + q * 16) + e;
       if (at < kCap) {
         sl.cap_id[r][at] = c * CH + q * VEC + e;
@@ -429,7 +435,7 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
   uint32_t diff = 0;
 #pragma unroll
   for (int h = 0; h < kVecs; ++h) {
-    const int q = h * kCT + tid;
+    const int q = vec_index(h, warp, lane);
     const uint4 a = lds128(starget + q * 16);
     unpack(a, vt[h], (In *)nullptr);
     if (PAIR) {
@@ -447,7 +453,7 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
     diff = 0;
 #pragma unroll
     for (int h = 0; h < kVecs; ++h) {
-      const int id0 = c * CH + (h * kCT + tid) * VEC;
+      const int id0 = c * CH + vec_index(h, warp, lane) * VEC;
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         if (id0 + e >= p.vocab_local) {
@@ -502,8 +508,9 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
 }
 
 // Sample item: per-tile fp64 sums of the residual / bonus weights. Tile
-// (chunk, h, warp) covers ids [chunk*CH + (h*kCT + warp*32)*VEC, +32*VEC):
-// tile index order is id order.
+// (chunk, warp) covers the warp's contiguous kVecs * 32 vectors of the chunk,
+// ids [chunk*CH + warp*kVecs*32*VEC, +kVecs*32*VEC): tile index order is id
+// order.
 template <class In>
 __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_t *starget,
                                              int chunk, const Weigher<typename InTraits<In>::Acc> &wf,
@@ -512,9 +519,10 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
+  double ls = 0.0;
 #pragma unroll
   for (int h = 0; h < kVecs; ++h) {
-    const int q = h * kCT + tid;
+    const int q = vec_index(h, warp, lane);
     const int id0 = chunk * CH + q * VEC;
     Acc vt[VEC], vd[VEC];
     unpack(lds128(starget + q * 16), vt, (In *)nullptr);
@@ -526,12 +534,13 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
     }
     Acc w[VEC];
     weigh_vec<VEC>(wf, vt, vd, w);
-    Acc ls = Acc(0);
+    Acc lv = Acc(0);
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) ls = add_rn(ls, (id0 + e < p.vocab_local) ? w[e] : Acc(0));
-    const double ts = warp_sum_f64((double)ls);
-    if (lane == 0) tiles[(chunk * kVecs + h) * kCW + warp] = ts;
+    for (int e = 0; e < VEC; ++e) lv = add_rn(lv, (id0 + e < p.vocab_local) ? w[e] : Acc(0));
+    ls += (double)lv;
   }
+  const double ts = warp_sum_f64(ls);
+  if (lane == 0) tiles[chunk * kCW + warp] = ts;
 }
 
 template <class In, bool NEEDZ>
@@ -815,7 +824,7 @@ __device__ __noinline__ void select_topm(Slot<typename InTraits<In>::Acc> &sl, i
       const int cc = blk / kCW, w = blk - cc * kCW;
 #pragma unroll 1
       for (int h = 0; h < kVecs; ++h) {
-        const int id0 = cc * CH + (h * kCT + w * 32 + lane) * VEC;
+        const int id0 = cc * CH + vec_index(h, w, lane) * VEC;
         Acc v[VEC];
 #pragma unroll
         for (int e = 0; e < VEC; ++e) v[e] = neg_inf<Acc>();
@@ -1040,20 +1049,15 @@ __device__ __forceinline__ void complete_item(const DevOut &o, const DevScratch 
   }
 }
 
-// Resolve the element of tile `t` that holds T (warp-cooperative re-read).
+// Weights of this lane's vector of one (chunk, warp, h) and their fp64 sum.
 template <class In>
-__device__ __noinline__ int resolve_tile(const In *rt, const In *rd,
-                                            const Weigher<typename InTraits<In>::Acc> &wf, int t,
-                                            double run, double T, double W, double eps,
-                                            const DevParams &p, int lane, int &near,
-                                            bool want_last) {
+__device__ __forceinline__ double vector_weights(const In *rt, const In *rd,
+                                                 const Weigher<typename InTraits<In>::Acc> &wf,
+                                                 int id0, const DevParams &p,
+                                                 typename InTraits<In>::Acc (&wt)[InTraits<In>::kVec]) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
-  constexpr int CH = kRowBytes / (int)sizeof(In);
-  const int c = t / (kVecs * kCW), r = t - c * kVecs * kCW;
-  const int h = r / kCW, w = r - h * kCW;
-  const int id0 = c * CH + (h * kCT + w * 32 + lane) * VEC;
-  Acc vt[VEC], vd[VEC], wt[VEC];
+  Acc vt[VEC], vd[VEC];
   const bool ok = id0 < p.vocab_local;
   if (ok) {
     unpack(ldg128(rt + id0), vt, (In *)nullptr);
@@ -1063,8 +1067,7 @@ __device__ __noinline__ int resolve_tile(const In *rt, const In *rd,
 #pragma unroll
       for (int e = 0; e < VEC; ++e) vd[e] = Acc(0);
     }
-  }
-  if (!ok) {
+  } else {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) vt[e] = vd[e] = Acc(0);
   }
@@ -1075,6 +1078,54 @@ __device__ __noinline__ int resolve_tile(const In *rt, const In *rd,
     if (!(ok && id0 + e < p.vocab_local)) wt[e] = Acc(0);
     ls += (double)wt[e];
   }
+  return ls;
+}
+
+// Resolve the element of tile `t` = (chunk, warp) that holds T
+// (warp-cooperative re-read): find the tile's vector whose running total
+// passes T, then the lane and the element inside it.
+template <class In>
+__device__ __noinline__ int resolve_tile(const In *rt, const In *rd,
+                                            const Weigher<typename InTraits<In>::Acc> &wf, int t,
+                                            double run, double T, double W, double eps,
+                                            const DevParams &p, int lane, int &near,
+                                            bool want_last) {
+  using Acc = typename InTraits<In>::Acc;
+  constexpr int VEC = InTraits<In>::kVec;
+  constexpr int CH = kRowBytes / (int)sizeof(In);
+  const int c = t / kCW, w = t - c * kCW;
+  int h = 0;
+  {
+    // the crossing vector of the tile (or, for the gap fallback, the last supported one)
+    int last = -1, found = -1;
+    double r = run;
+#pragma unroll
+    for (int hh = 0; hh < kVecs; ++hh) {
+      Acc tmp[VEC];
+      const double vs = warp_sum_f64(
+          vector_weights<In>(rt, rd, wf, c * CH + vec_index(hh, w, lane) * VEC, p, tmp));
+      if (vs > 0.0) last = hh;
+      if (found < 0 && vs > 0.0 && r + vs > T) found = hh;
+      if (found < 0) r += vs;
+    }
+    if (want_last || found < 0) {
+      h = last < 0 ? kVecs - 1 : last;
+      want_last = true;
+    } else {
+      h = found;
+      // run before vector h
+      double rr = run;
+      for (int hh = 0; hh < h; ++hh) {
+        Acc tmp[VEC];
+        rr += warp_sum_f64(
+            vector_weights<In>(rt, rd, wf, c * CH + vec_index(hh, w, lane) * VEC, p, tmp));
+      }
+      run = rr;
+    }
+  }
+  const int id0 = c * CH + vec_index(h, w, lane) * VEC;
+  Acc wt[VEC];
+  const double ls = vector_weights<In>(rt, rd, wf, id0, p, wt);
   int result = -1;
   if (want_last) {
     // rounding-gap fallback: the last supported id of this tile
@@ -1206,7 +1257,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
   const int G1 = p.gamma + 1;
   const int M = p.top_m;
   const double omt_d = (double)p.omt_f, tau_d = (double)p.tau_f;
-  const int nblocks = p.n_chunks * kVecs * kCW;
+  const int nblocks = p.n_chunks * kCW;  // sample tiles (chunk, warp)
   unsigned long long *trl = lane == 0 ? tr : nullptr;
   for (int n = ew;; n += kEW) {
     const int si = n % kSlots;
@@ -1563,7 +1614,7 @@ cudaError_t launch_fused(const DevParams &p, const void *draft, const void *targ
   constexpr int CH = fz::kRowBytes / (int)sizeof(In);
   DevParams q = p;
   q.n_chunks = (p.vocab_local + CH - 1) / CH;
-  const int ntiles = q.n_chunks * fz::kVecs * fz::kCW;
+  const int ntiles = q.n_chunks * fz::kCW;
   if (ntiles > fz::kMaxTiles || 8 * q.n_chunks * fz::kCW > fz::kAreaBytes)
     return cudaErrorInvalidValue;
   const size_t smem = sizeof(fz::Smem<Acc>);
@@ -1597,7 +1648,7 @@ cudaError_t launch_fused(const DevParams &p, const void *draft, const void *targ
 // sample tiles, must fit the slot area).
 int fused_max_vocab(int esize, int top_m) {
   (void)top_m;
-  const int by_tiles = fz::kMaxTiles / (fz::kVecs * fz::kCW);
+  const int by_tiles = fz::kMaxTiles / fz::kCW;
   const int by_area = fz::kAreaBytes / (8 * fz::kCW);
   const int chunks = by_tiles < by_area ? by_tiles : by_area;
   return chunks * (fz::kRowBytes / esize);
