@@ -1,0 +1,145 @@
+// Does heavy ALU/MUFU work in 16 consumer warps slow the TMA stream that
+// feeds them? (development aid). Producer: 1 warp, 1-D bulk copies of two
+// 16 KB halves per stage into an S-stage ring, a global ticket over a 1 GB
+// buffer. Consumers: per stage, `work` iterations of an FFMA2 + MUFU mix
+// shaped like the verifier's fold. Reports GB/s with copies, and the time of
+// the same consumer work with the copies skipped (compute only).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t sa(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void wait(uint64_t *b, uint32_t ph) {
+  uint32_t d = 0;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                 : "=r"(d) : "r"(sa(b)), "r"(ph) : "memory");
+  } while (!d);
+}
+
+__global__ void __launch_bounds__(17 * 32, 1)
+    kern(const uint8_t *src, size_t total, int stages, int work, int copy, unsigned *ticket,
+         float *sink, int rowwise, int vary) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int SB = 32768;
+  uint64_t *full = (uint64_t *)(sm + (size_t)SB * stages);
+  uint64_t *empty = full + 16;
+  long long *chunk_of = (long long *)(empty + 16);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&empty[i])), "r"(16));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  const size_t nchunks = total / SB;
+  if (warp == 16) {
+    if (lane == 0) {
+      int st = 0; uint32_t ph = 0;
+      size_t item = 0;
+      int k = 16;
+      for (;;) {
+        size_t c;
+        if (rowwise) {
+          // like the verifier: claim a row pair, stream its 16 chunks in order
+          if (k == 16) { item = atomicAdd(ticket, 1u); k = 0; }
+          c = item * 16 + k++;
+        } else {
+          c = atomicAdd(ticket, 1u);
+        }
+        wait(&empty[st], ph ^ 1);
+        chunk_of[st] = c < nchunks ? (long long)c : -1;
+        if (c >= nchunks) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&full[st])) : "memory");
+          break;
+        }
+        if (copy) {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[st])), "r"(SB) : "memory");
+          const int half = SB / 2;
+          // two rows far apart, like a (draft, target) row pair
+          const uint8_t *a, *b;
+          if (rowwise) {  // rows of 256 KB: draft row in the first half, target row in the second
+            a = src + (item * 262144 + (c % 16) * half) % (total / 2);
+            b = src + total / 2 + (item * 262144 + (c % 16) * half) % (total / 2);
+          } else {
+            a = src + (c * half) % (total / 2);
+            b = src + total / 2 + (c * half) % (total / 2);
+          }
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(sm + (size_t)st * SB)), "l"(a), "r"(half), "r"(sa(&full[st])) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(sm + (size_t)st * SB + half)), "l"(b), "r"(half), "r"(sa(&full[st])) : "memory");
+        } else {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&full[st])) : "memory");
+        }
+        if (++st == stages) { st = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+  int st = 0; uint32_t ph = 0;
+  float acc = 0.f;
+  unsigned long long p = 0x3f8000003f800000ull;
+  const unsigned long long m = 0x3f7fbe773f7fbe77ull, cc = 0x3a83126f3a83126full;
+  for (;;) {
+    wait(&full[st], ph);
+    if (chunk_of[st] < 0) break;
+    // read the whole stage like the fold does (4 x LDS.128 per thread)
+    float x = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = *(const uint4 *)(sm + (size_t)st * SB + (q * 512 + threadIdx.x) * 16);
+      x += __uint_as_float(v.x ^ v.y ^ v.z ^ v.w) * 1e-30f;
+    }
+    // per-warp, per-chunk variable work (like capture calls): work * (0.5 .. 1.5)
+    const unsigned hsh = (unsigned)(chunk_of[st] * 2654435761ull) ^ (warp * 40503u);
+    const int wk = vary ? work / 2 + (int)((hsh >> 7) % (unsigned)(work + 1)) : work;
+    for (int i = 0; i < wk; ++i) {
+      float y;
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p) : "l"(m), "l"(cc));
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p) : "l"(m), "l"(cc));
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p) : "l"(m), "l"(cc));
+      acc += y;
+      x = y * 1e-3f;
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[st])) : "memory");
+    if (++st == stages) { st = 0; ph ^= 1; }
+  }
+  if (acc == 12345.f) sink[0] = acc + (float)p;
+}
+
+int main() {
+  const size_t total = (size_t)1 << 30;
+  uint8_t *src; unsigned *ticket; float *sink;
+  cudaMalloc(&src, total); cudaMemset(src, 1, total);
+  cudaMalloc(&ticket, 4); cudaMalloc(&sink, 4);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int works[] = {48};
+  for (int vary : {0, 1})
+  for (int rowwise : {1})
+  for (int stages : {3, 5, 8}) {
+    const size_t smem = (size_t)32768 * stages + 1024;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int w : works) {
+      float t[2];
+      for (int copy = 1; copy >= 0; --copy) {
+        float best = 1e9f;
+        for (int rep = 0; rep < 3; ++rep) {
+          cudaMemset(ticket, 0, 4);
+          cudaEventRecord(e0);
+          kern<<<148, 17 * 32, smem>>>(src, total, stages, w, copy, ticket, sink, rowwise, vary);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms; cudaEventElapsedTime(&ms, e0, e1);
+          if (ms < best) best = ms;
+        }
+        t[copy] = best;
+      }
+      printf("vary %d rowwise %d stages %d work %3d: with copies %.3f ms (%6.0f GB/s), compute only %.3f ms, err=%s\n",
+             vary, rowwise, stages, w, t[1], total / t[1] / 1e6, t[0], cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}
