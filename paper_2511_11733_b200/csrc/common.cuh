@@ -177,23 +177,37 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
 
 // 2^x on the FMA pipe for two lanes at once (offloads the MUFU unit):
 // x = n + f with n = rint(x) (1.5*2^23 magic), f in [-0.5, 0.5];
-// 2^f by a degree-5 relative-minimax polynomial (max rel. error 2.3e-7 in fp32
-// Horner, cf. ex2.approx's ~1.2e-7), scaled by 2^n through the exponent field.
-// x is clamped below at -127 (results under 2^-127 are negligible, like ex2.approx.ftz).
+// 2^f by a relative-minimax polynomial (degree 4: max rel. error 2.7e-6 in
+// fp32 Horner; -DDSDV_POLY5: degree 5, 2.3e-7), scaled by 2^n through the
+// exponent field.
+// x is clamped below at -126 (results under 2^-126 are negligible, like ex2.approx.ftz).
 __device__ __forceinline__ f32x2 poly_exp2x2(f32x2 x) {
   // callers guarantee x <= ~12 (lazy-max slack); only the low end needs a clamp
-  const float a = fmaxf(lo2(x), -127.0f);
-  const float b = fmaxf(hi2(x), -127.0f);
+  // clamp at -126: with n >= -126 the exponent add cannot wrap even when the
+  // polynomial dips just below 1 at f = 0
+  const float a = fmaxf(lo2(x), -126.0f);
+  const float b = fmaxf(hi2(x), -126.0f);
   const f32x2 xc = pk2(a, b);
   const f32x2 magic = pk2(12582912.0f, 12582912.0f);
   const f32x2 j = add2(xc, magic);
   const f32x2 f = sub2(xc, sub2(j, magic));
+#ifdef DSDV_POLY5
   f32x2 p = fma2(pk2(1.327647129073739e-3f, 1.327647129073739e-3f), f,
                  pk2(9.675540961325169e-3f, 9.675540961325169e-3f));
   p = fma2(p, f, pk2(5.550713092088699e-2f, 5.550713092088699e-2f));
   p = fma2(p, f, pk2(2.4022120237350464e-1f, 2.4022120237350464e-1f));
   p = fma2(p, f, pk2(6.931469440460205e-1f, 6.931469440460205e-1f));
   p = fma2(p, f, pk2(1.0000001192092896f, 1.0000001192092896f));
+#else
+  // degree 4: max relative error 2.7e-6 in fp32 Horner — within the 1e-5
+  // tolerance on softened probabilities (the mix sum's relative error is at
+  // most the per-term one), one FFMA2 per element pair cheaper
+  f32x2 p = fma2(pk2(9.570101276040077e-3f, 9.570101276040077e-3f), f,
+                 pk2(5.591785907745361e-2f, 5.591785907745361e-2f));
+  p = fma2(p, f, pk2(2.40247443318367e-1f, 2.40247443318367e-1f));
+  p = fma2(p, f, pk2(6.931217908859253e-1f, 6.931217908859253e-1f));
+  p = fma2(p, f, pk2(9.999992847442627e-1f, 9.999992847442627e-1f));
+#endif
   const unsigned jl = __float_as_uint(lo2(j)), jh = __float_as_uint(hi2(j));
   const float rl = __uint_as_float(__float_as_uint(lo2(p)) + (jl << 23));
   const float rh = __uint_as_float(__float_as_uint(hi2(p)) + (jh << 23));
