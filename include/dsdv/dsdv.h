@@ -221,6 +221,12 @@ dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t 
                               const double *uniform, const double *masses_all, double *mass_out,
                               int32_t *token_out, int32_t *status, void *stream);
 
+/* ---- pipeline emulation -------------------
+ * Holds `stream` for `nanoseconds` of device time (%globaltimer): the compute
+ * step t0 of a stage or the injected latency t1 of a link, replacing the
+ * reference's simulated delays (netsim.cpp:110-172) with device time. */
+dsdv_status dsdv_spin(dsdv_ctx *ctx, uint64_t nanoseconds, void *stream);
+
 /* ---- helpers ----------------------------------------------------------- */
 /* The accept / extra / draft uniform the kernels use (philox.h), on the host. */
 double dsdv_uniform(uint64_t seed, uint64_t window, uint32_t sequence, uint32_t slot);

@@ -33,6 +33,7 @@ cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nran
                                 int32_t *status, cudaStream_t stream);
 cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, double tau,
                             double *out, int32_t *status, cudaStream_t stream);
+cudaError_t launch_spin(unsigned long long ns, cudaStream_t stream);
 cudaError_t launch_synth(int dtype, int B, int gamma, int V, int stride, uint64_t seed,
                          void *draft, void *target, cudaStream_t stream);
 }  // namespace dsdv
@@ -478,6 +479,16 @@ dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t 
       break;
   }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "shard_sample launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_spin(dsdv_ctx *ctx, uint64_t nanoseconds, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  e = dsdv::launch_spin((unsigned long long)nanoseconds, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "spin launch");
   ctx->launches += 1;
   return DSDV_OK;
 }

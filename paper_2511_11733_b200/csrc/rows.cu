@@ -287,6 +287,22 @@ __global__ void __launch_bounds__(1024) mix_rows_kernel(int kind, int V, const d
   if (threadIdx.x == 0) *status = DSDV_OK;
 }
 
+// Pipeline emulation: one thread holds the stream for `ns`
+// nanoseconds of %globaltimer — a stage's compute step t0 or a link's
+// injected latency t1.
+__global__ void spin_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+cudaError_t launch_spin(unsigned long long ns, cudaStream_t stream) {
+  spin_kernel<<<1, 1, 0, stream>>>(ns);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, double tau,
                             double *out, int32_t *status, cudaStream_t stream) {
   mix_rows_kernel<<<1, 1024, 0, stream>>>(kind, V, a, b, tau, out, status);

@@ -88,6 +88,7 @@ def _load() -> C.CDLL:
         "dsdv_shard_sample": (st, [vp, C.POINTER(_Params), C.c_int32, C.c_int32, C.c_int32, vp,
                                    vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "dsdv_mix_rows": (st, [vp, C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp, vp]),
+        "dsdv_spin": (st, [vp, C.c_uint64, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -100,7 +101,8 @@ LIB = _load()
 EXPORTED = ("dsdv_create", "dsdv_destroy", "dsdv_last_error", "dsdv_abi_version", "dsdv_validate",
             "dsdv_verify", "dsdv_window_stats", "dsdv_sample_extra", "dsdv_draft_sample",
             "dsdv_sync", "dsdv_uniform", "dsdv_synth_logits", "dsdv_launch_count",
-            "dsdv_shard_stats", "dsdv_shard_merge", "dsdv_shard_sample", "dsdv_mix_rows")
+            "dsdv_shard_stats", "dsdv_shard_merge", "dsdv_shard_sample", "dsdv_mix_rows",
+            "dsdv_spin")
 
 
 def uniform(seed: int, window: int, sequence: int, slot: int) -> float:
@@ -299,6 +301,11 @@ class Verifier:
         self._check(LIB.dsdv_synth_logits(self._h, C.byref(cp), logits_seed, draft.data_ptr(),
                                           target.data_ptr(), s))
         return draft, target
+
+    def spin(self, nanoseconds: int, stream=None) -> None:
+        """dsdv_spin: hold the stream for `nanoseconds` of device time."""
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._check(LIB.dsdv_spin(self._h, int(nanoseconds), s))
 
     def sync(self, p: VerifyParams | None = None, out: WindowResult | None = None,
              batch: int = 0, vocab: int = 2, stream=None):

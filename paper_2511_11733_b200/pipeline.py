@@ -1,0 +1,132 @@
+"""Pipeline-sharded decoding emulation.
+
+The reference models an N-node pipeline where every committed unit pays its
+compute and then one synchronization round of N-1 sequential link hops
+(`run_pipeline`, netsim.cpp:110-172; closed forms latency.cpp:63-86):
+
+    standard decoding  one unit per token:       t0 + (N-1) t1
+    DSD                one unit per window:      k t0 + (N-1) t1, commits k + 1
+
+This module measures the same thing on GPUs: stage s of the N logical stages
+lives on GPU s mod P; a unit is a device spin of its compute time on the GPU of
+stage 0, then for every link an injected device spin of t1 followed by a
+send/recv of the committed token ids to the next stage's GPU (NCCL when the
+stages sit on different GPUs), and finally the commit returns to stage 0
+(the next unit's input). The k values come from the GPU verifier. Reported:
+measured R_comm = 1 - T_dsd / T_std over equal committed tokens, the
+analytic comm_reduction_ratio at the mean committed length, the reference's
+deterministic DES totals and the synchronization-round counts.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+# ---- closed forms (latency.cpp:63-86) -------------------------------------
+def sync_cost(n_nodes: int, t1: float) -> float:
+    return (n_nodes - 1) * t1
+
+
+def standard_decode_time(tokens: float, n_nodes: int, t0: float, t1: float) -> float:
+    return tokens * (t0 + sync_cost(n_nodes, t1))
+
+
+def dsd_round_time(tokens: float, n_nodes: int, t0: float, t1: float) -> float:
+    return tokens * t0 + sync_cost(n_nodes, t1)
+
+
+def comm_reduction_ratio(tokens: float, n_nodes: int, t0: float, t1: float) -> float:
+    return sync_cost(n_nodes, t1) * (tokens - 1.0) / (tokens * (t0 + sync_cost(n_nodes, t1)))
+
+
+# ---- the reference's pipeline with constant link latency ------------------
+@dataclass
+class Unit:
+    compute: float  # time units
+    tokens: int     # committed by the unit
+
+
+def standard_units(n_tokens: int, t0: float) -> list[Unit]:
+    """simulate_standard (netsim.cpp:176-185): one unit per token."""
+    return [Unit(t0, 1) for _ in range(n_tokens)]
+
+
+def dsd_units(ks: list[int], t0: float) -> list[Unit]:
+    """simulate_dsd (netsim.cpp:187-202): compute k t0, commit k + 1."""
+    return [Unit(k * t0, k + 1) for k in ks]
+
+
+def des_total(units: list[Unit], n_nodes: int, t1: float) -> float:
+    """run_pipeline with a constant link sampler: units strictly sequential,
+    each computes then crosses the N-1 links one after another."""
+    now = 0.0
+    for u in units:
+        now += u.compute
+        for _ in range(n_nodes - 1):
+            now += t1
+    return now
+
+
+# ---- the device emulation --------------------------------------------------
+class PipelineEmulator:
+    """Runs units over N logical stages on the `comm` ranks (stage s on rank
+    s mod P). `verifier` supplies dsdv_spin on this rank's device; `comm` is a
+    torch.distributed process group wrapper (None for one GPU)."""
+
+    def __init__(self, verifier, n_stages: int, comm=None):
+        import torch
+        self.torch = torch
+        self.v = verifier
+        self.N = n_stages
+        self.comm = comm
+        self.P = comm.size if comm else 1
+        self.rank = comm.rank if comm else 0
+        self.payload = torch.zeros(16, dtype=torch.int32, device=torch.device("cuda", verifier.device))
+
+    def owner(self, s: int) -> int:
+        return s % self.P
+
+    def _send(self, dst: int):
+        self.comm.dist.send(self.payload, dst)
+
+    def _recv(self, src: int):
+        self.comm.dist.recv(self.payload, src)
+
+    def run(self, units: list[Unit], t1_ns: int) -> float:
+        """Executes the units (compute in ns); returns elapsed device
+        milliseconds (max over ranks when distributed)."""
+        torch = self.torch
+        dev = torch.device("cuda", self.v.device)
+        if self.comm:
+            self.comm.dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for u in units:
+            for s in range(self.N):
+                if self.owner(s) != self.rank:
+                    continue
+                if s == 0:
+                    if u.compute > 0:
+                        self.v.spin(int(u.compute))  # the unit's compute (ns)
+                else:
+                    if self.P > 1:
+                        self._recv(self.owner(s - 1))
+                if s < self.N - 1:
+                    self.v.spin(t1_ns)
+                    if self.P > 1:
+                        self._send(self.owner(s + 1))
+            # back edge: the committed tokens return to stage 0 for the next unit
+            if self.P > 1 and self.owner(self.N - 1) != self.owner(0):
+                if self.rank == self.owner(self.N - 1):
+                    self._send(self.owner(0))
+                elif self.rank == self.owner(0):
+                    self._recv(self.owner(self.N - 1))
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        if self.comm:
+            t = torch.tensor([ms], device=dev)
+            self.comm.all_reduce_max(t)
+            ms = float(t.item())
+        return ms
