@@ -191,8 +191,8 @@ dsdv_status dsdv_sync(dsdv_ctx *ctx, const dsdv_params *params, const int32_t *s
  * Per window, with the caller's collectives in between (csrc/shard.cu):
  *   dsdv_shard_stats   -> all-gather records [P][B][gamma+1][DSDV_RECORD_WORDS]
  *                         and top lists [P][B][gamma][2][m] (m = min(top_m, V))
- *   dsdv_shard_merge   (identical on every rank: k, key flags, accept draws)
- *   dsdv_shard_sample(DSDV_SHARD_MASS)    -> all-gather the [B] masses
+ *   dsdv_shard_merge   (identical on every rank: k, key flags, accept draws;
+ *                       this slice's mass of the extra row) -> all-gather [B] masses
  *   dsdv_shard_sample(DSDV_SHARD_RESOLVE) -> all-reduce(max) the [B] tokens
  * Decisions equal the unsharded verifier's except inside the eps bands (the
  * merged fp32 sums are re-associated). */
@@ -200,16 +200,25 @@ dsdv_status dsdv_shard_stats(dsdv_ctx *ctx, const dsdv_params *params, const voi
                              const void *target_logits, const int32_t *draft_tokens,
                              double *records, double *top_values, int32_t *top_ids,
                              void *stream);
-/* out: per-sequence outputs (extra_token is set to -1 until the resolve step),
+/* rank_stride_bytes: 0 when the three gathered arrays are each [nranks][...]
+ * contiguous; else the byte distance between consecutive ranks' copies of
+ * all three (one packed exchange buffer per rank, one all-gather).
+ * out: per-sequence outputs (extra_token is set to -1 until the resolve step),
  * optional per-position outputs, and out->records (required) receives the
  * merged global records. position[b] = the row of the extra draw (k for a
  * residual, gamma for the bonus, -1 when the sequence stopped on an error);
- * uniform[b] = its Philox draw. */
+ * uniform[b] = its Philox draw; mass_out[b] = this slice's weight total of
+ * that row (the MASS step, fused; gamma <= 31). tile_scratch (optional,
+ * [B][DSDV_SHARD_TILE_WORDS] doubles) keeps the row's tile sums so that the
+ * RESOLVE step of the owning rank re-reads one tile instead of the slice. */
+#define DSDV_SHARD_TILE_WORDS 514
 dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
                              const double *records_all, const double *top_values_all,
-                             const int32_t *top_ids_all, const int32_t *draft_tokens,
-                             const dsdv_outputs *out, int32_t *position, double *uniform,
-                             void *stream);
+                             const int32_t *top_ids_all, uint64_t rank_stride_bytes,
+                             const void *draft_logits, const void *target_logits,
+                             const int32_t *draft_tokens, const dsdv_outputs *out,
+                             int32_t *position, double *uniform, double *mass_out,
+                             double *tile_scratch, void *stream);
 enum { DSDV_SHARD_MASS = 0, DSDV_SHARD_RESOLVE = 1 };
 /* MASS: mass_out[b] = this slice's weight total of row position[b].
  * RESOLVE: masses_all = the gathered [nranks][B] totals; token_out[b] = the
@@ -219,7 +228,8 @@ dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t 
                               int32_t nranks, const void *draft_logits, const void *target_logits,
                               const double *records, const int32_t *position,
                               const double *uniform, const double *masses_all, double *mass_out,
-                              int32_t *token_out, int32_t *status, void *stream);
+                              int32_t *token_out, int32_t *status, const double *tile_scratch,
+                              void *stream);
 
 /* ---- pipeline emulation -------------------
  * Holds `stream` for `nanoseconds` of device time (%globaltimer): the compute

@@ -22,15 +22,18 @@ cudaError_t launch_sample_extra(const DevParams &, const void *, const void *, c
                                 cudaStream_t);
 template <class In>
 cudaError_t launch_draft_sample(const DevParams &, const void *, int32_t *, cudaStream_t);
+template <class In>
 cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const double *topv,
-                               const int32_t *topi, int P, const int32_t *tokens, const DevOut &o,
-                               int32_t *position, double *uniform, cudaStream_t stream);
+                               const int32_t *topi, int P, size_t rank_bytes, const void *draft,
+                               const void *target, const int32_t *tokens, const DevOut &o,
+                               int32_t *position, double *uniform, double *mass_out,
+                               double *tiles, cudaStream_t stream);
 template <class In>
 cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nranks,
                                 const void *draft, const void *target, const double *records,
                                 const int32_t *position, const double *uniform,
                                 const double *masses, double *mass_out, int32_t *token_out,
-                                int32_t *status, cudaStream_t stream);
+                                int32_t *status, const double *tiles, cudaStream_t stream);
 cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, double tau,
                             double *out, int32_t *status, cudaStream_t stream);
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t stream);
@@ -418,15 +421,18 @@ dsdv_status dsdv_shard_stats(dsdv_ctx *ctx, const dsdv_params *params, const voi
 
 dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
                              const double *records_all, const double *top_values_all,
-                             const int32_t *top_ids_all, const int32_t *draft_tokens,
-                             const dsdv_outputs *out, int32_t *position, double *uniform,
-                             void *stream) {
+                             const int32_t *top_ids_all, uint64_t rank_stride_bytes,
+                             const void *draft_logits, const void *target_logits,
+                             const int32_t *draft_tokens, const dsdv_outputs *out,
+                             int32_t *position, double *uniform, double *mass_out,
+                             double *tile_scratch, void *stream) {
   if (!ctx) return DSDV_E_INVARIANT;
   DevParams d;
   dsdv_status st = build_params(ctx, params, d);
   if (st != DSDV_OK) return st;
   if (!records_all || !top_values_all || !top_ids_all || !draft_tokens || !out || !position ||
-      !uniform || !out->records || !out->accepted_count || !out->extra_token ||
+      !uniform || !mass_out || !draft_logits || !target_logits || !out->records ||
+      !out->accepted_count || !out->extra_token ||
       !out->extra_source || !out->key_count || !out->status || !out->near_threshold)
     return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_merge: null argument");
   if (nranks < 1 || nranks > 64)
@@ -434,8 +440,26 @@ dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t n
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
   const DevOut o = to_dev(out);
-  e = dsdv::launch_shard_merge(d, records_all, top_values_all, top_ids_all, nranks, draft_tokens,
-                               o, position, uniform, (cudaStream_t)stream);
+  switch (params->dtype) {
+    case DSDV_DTYPE_BF16:
+      e = dsdv::launch_shard_merge<__nv_bfloat16>(d, records_all, top_values_all, top_ids_all,
+                                                  nranks, (size_t)rank_stride_bytes, draft_logits,
+                                                  target_logits, draft_tokens, o, position,
+                                                  uniform, mass_out, tile_scratch, (cudaStream_t)stream);
+      break;
+    case DSDV_DTYPE_F32:
+      e = dsdv::launch_shard_merge<float>(d, records_all, top_values_all, top_ids_all, nranks,
+                                          (size_t)rank_stride_bytes, draft_logits, target_logits,
+                                          draft_tokens, o, position, uniform, mass_out,
+                                          tile_scratch, (cudaStream_t)stream);
+      break;
+    default:
+      e = dsdv::launch_shard_merge<double>(d, records_all, top_values_all, top_ids_all, nranks,
+                                           (size_t)rank_stride_bytes, draft_logits, target_logits,
+                                           draft_tokens, o, position, uniform, mass_out,
+                                           tile_scratch, (cudaStream_t)stream);
+      break;
+  }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "shard_merge launch");
   ctx->launches += 1;
   return DSDV_OK;
@@ -445,7 +469,8 @@ dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t 
                               int32_t nranks, const void *draft_logits, const void *target_logits,
                               const double *records, const int32_t *position,
                               const double *uniform, const double *masses_all, double *mass_out,
-                              int32_t *token_out, int32_t *status, void *stream) {
+                              int32_t *token_out, int32_t *status, const double *tile_scratch,
+                              void *stream) {
   if (!ctx) return DSDV_E_INVARIANT;
   DevParams d;
   dsdv_status st = build_params(ctx, params, d);
@@ -465,17 +490,17 @@ dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t 
       e = dsdv::launch_shard_sample<__nv_bfloat16>(d, mode, rank, nranks, draft_logits,
                                                    target_logits, records, position, uniform,
                                                    masses_all, mass_out, token_out, status,
-                                                   (cudaStream_t)stream);
+                                                   tile_scratch, (cudaStream_t)stream);
       break;
     case DSDV_DTYPE_F32:
       e = dsdv::launch_shard_sample<float>(d, mode, rank, nranks, draft_logits, target_logits,
                                            records, position, uniform, masses_all, mass_out,
-                                           token_out, status, (cudaStream_t)stream);
+                                           token_out, status, tile_scratch, (cudaStream_t)stream);
       break;
     default:
       e = dsdv::launch_shard_sample<double>(d, mode, rank, nranks, draft_logits, target_logits,
                                             records, position, uniform, masses_all, mass_out,
-                                            token_out, status, (cudaStream_t)stream);
+                                            token_out, status, tile_scratch, (cudaStream_t)stream);
       break;
   }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "shard_sample launch");

@@ -183,7 +183,9 @@ __device__ __forceinline__ void vec_weights(const uint4 &rt, const uint4 &rd, in
 template <class In, class Acc>
 __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const Weigher<Acc> &wf_s,
                                        int n, double u, double eps, SampleShared *sh, int tid,
-                                       int *near_out, double t_override = -1.0) {
+                                       int *near_out, double t_override = -1.0,
+                                       double *tiles_out = nullptr,
+                                       const double *tiles_in = nullptr) {
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int U = 4;  // tiles in flight per warp
   const Weigher<Acc> wf = wf_s;
@@ -197,10 +199,21 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
   const int t0 = min(ntiles, warp * per_warp);
   const int t1 = min(ntiles, t0 + per_warp);
 
-  // ---- one pass: tile sums -> shared memory ----
+  // ---- one pass: tile sums -> shared memory (or the sums a previous call
+  // over the same row and weights saved: tiles_in = [kMaxTiles] sums, W, last) ----
   int last = -1;
   double wsum = 0.0;
-  for (int t = t0; t < t1; t += U) {
+  if (tiles_in) {
+    for (int t = tid; t < ntiles; t += kConsumerThreads) sh->tile[t] = tiles_in[t];
+    if (tid == 0) {
+      sh->warp_total[0] = tiles_in[kMaxTiles];
+      sh->warp_last[0] = (int)tiles_in[kMaxTiles + 1];
+    } else if (tid < kConsumerWarps) {
+      sh->warp_total[tid] = 0.0;
+      sh->warp_last[tid] = -1;
+    }
+  }
+  for (int t = tiles_in ? t1 : t0; t < t1; t += U) {
     double ls[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) ls[k] = 0.0;
@@ -238,7 +251,7 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-  if (lane == 0) {
+  if (lane == 0 && !tiles_in) {
     sh->warp_total[warp] = wsum;
     sh->warp_last[warp] = last;
   }
@@ -274,6 +287,13 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
         base = run + __shfl_sync(0xffffffffu, incl - x, src);
       }
       run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tiles_out) {
+      for (int t = lane; t < ntiles; t += 32) tiles_out[t] = sh->tile[t];
+      if (lane == 0) {
+        tiles_out[kMaxTiles] = W;
+        tiles_out[kMaxTiles + 1] = (double)L;
+      }
     }
     if (lane == 0) {
       sh->W = W;

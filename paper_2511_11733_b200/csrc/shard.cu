@@ -31,97 +31,142 @@ namespace dsdv {
 constexpr int kMaxShards = 64;
 
 struct MergeIn {
-  const double *rec;   // [P][B][G1][kRecordWords] partial records
-  const double *topv;  // [P][B][G][2][M]
+  const double *rec;   // rank 0's [B][G1][kRecordWords] partial records
+  const double *topv;  // rank 0's [B][G][2][M]
   const int32_t *topi;
   int P;
+  // elements between consecutive ranks' copies (packed exchange buffers put
+  // all three arrays of one rank side by side)
+  size_t rec_stride, topv_stride, topi_stride;
 };
 
-__device__ __forceinline__ void lse_add(double &m, double &s, double x) {
-  // running log-sum-exp as (max, sum of exp(x - max))
-  if (x == -INFINITY) return;
-  if (x > m) {
-    s = (m == -INFINITY ? 0.0 : s * exp(m - x)) + 1.0;
-    m = x;
-  } else {
-    s += exp(x - m);
-  }
-}
+// One CTA per sequence, one warp per position (max(256, 32 (gamma+1))
+// threads): each warp merges its position's P slice records with warp
+// reductions and the top-m overlap with a warp-parallel ranking, lane 0 runs
+// the fp64 decision; warp 0 then finds the first rejection (verifier.cpp:
+// 223-250), and the CTA's first 256 threads compute this slice's mass of the
+// extra-draw row (the MASS step of dsdv_shard_sample, fused).
+struct PosSummary {
+  int err, key, kind, near, accepted;
+};
 
-// P-way merge of the slices' sorted top-M lists of one row into the global
-// top M ids (value desc, id asc; padding entries have id -1).
-__device__ __forceinline__ void merge_top(const MergeIn &in, size_t list_off, size_t stride_p,
-                                          int M, int *out) {
-  int ptr[kMaxShards];
-  for (int q = 0; q < in.P; ++q) ptr[q] = 0;
-  for (int r = 0; r < M; ++r) {
-    int best = -1;
-    double bv = 0.0;
-    int bid = 0;
-    for (int q = 0; q < in.P; ++q) {
-      if (ptr[q] >= M) continue;
-      const size_t at = q * stride_p + list_off + ptr[q];
-      const int id = in.topi[at];
-      if (id < 0) continue;
-      const double v = in.topv[at];
-      if (best < 0 || v > bv || (v == bv && id < bid)) {
-        best = q;
-        bv = v;
-        bid = id;
-      }
-    }
-    out[r] = best < 0 ? -1 : bid;
-    if (best >= 0) ++ptr[best];
-  }
-}
-
-// One warp per sequence; lane j evaluates position j (and the bonus row).
-__global__ void __launch_bounds__(128)
+template <class In>
+__global__ void __launch_bounds__(1024)
     shard_merge_kernel(const __grid_constant__ DevParams p, const MergeIn in,
+                       const In *__restrict__ draft, const In *__restrict__ target,
                        const int32_t *__restrict__ tokens, const DevOut o,
-                       int32_t *__restrict__ position, double *__restrict__ uniform) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= p.B) return;
-  const int b = warp;
+                       int32_t *__restrict__ position, double *__restrict__ uniform,
+                       double *__restrict__ mass_out, double *__restrict__ tiles) {
+  using Acc = typename InTraits<In>::Acc;
+  __shared__ PosSummary summ[32];
+  __shared__ int tset[32][kMaxTopM];
+  __shared__ SampleShared samp;
+  __shared__ Weigher<Acc> wf;
+  __shared__ int s_pos;
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = p.gamma, G1 = G + 1, M = p.top_m;
   const double omt = (double)p.omt_f, tau = (double)p.tau_f;
-  const size_t rec_stride_p = (size_t)p.B * G1 * kRecordWords;
-  const size_t top_stride_p = (size_t)p.B * G * 2 * M;
-  // sequence-level scan state
-  int k = G, keys = 0, nears = 0, stop_err = 0, stop_kind = 0;
-  for (int j0 = 0; j0 < G1; j0 += 32) {
-    const int j = j0 + lane;
-    const bool active = j < G1;
+  if (warp < G1) {
+    const int j = warp;
     const bool pair = j < G;
-    int err = 0, key = 0, kind = DSDV_EFF_TARGET, near = 0, accepted = 0;
-    if (active) {
-      // ---- merge the slices' normalisers ----
-      double mt = -INFINITY, md = -INFINITY, lt_m = -INFINITY, lt_s = 0.0, ld_m = -INFINITY,
-             ld_s = 0.0, lz_m = -INFINITY, lz_s = 0.0, lt_y = NAN, ld_y = NAN;
-      int diff = 0, own = 0;
-      for (int q = 0; q < in.P; ++q) {
-        const double *r = in.rec + q * rec_stride_p + ((size_t)b * G1 + j) * kRecordWords;
-        const double lt = r[0] + r[1];
-        lse_add(lt_m, lt_s, lt);
-        if (lt > -INFINITY) mt = fmax(mt, r[0]);
-        if (pair) {
-          const double ld = r[2] + r[3];
-          lse_add(ld_m, ld_s, ld);
-          if (ld > -INFINITY) md = fmax(md, r[2]);
-          lse_add(lz_m, lz_s, omt * r[0] + tau * r[2] + r[4]);
-          const int f = (int)r[7];
-          diff |= f & 1;
-          if (f & 2) {
-            own = 1;
-            lt_y = r[5];
-            ld_y = r[6];
-          }
+    // ---- normalisers: lanes over slices, log-sum-exp by warp reduction ----
+    double lt = -INFINITY, ld = -INFINITY, lz = -INFINITY, mtq = -INFINITY, mdq = -INFINITY;
+    double lty = NAN, ldy = NAN;
+    int f = 0;
+    for (int q = lane; q < in.P; q += 32) {
+      const double *r = in.rec + q * in.rec_stride + ((size_t)b * G1 + j) * kRecordWords;
+      const double a_t = r[0] + r[1];
+      if (a_t > -INFINITY) mtq = fmax(mtq, r[0]);
+      double m = fmax(lt, a_t);
+      lt = (m == -INFINITY) ? -INFINITY : m + log(exp(lt - m) + exp(a_t - m));
+      if (pair) {
+        const double a_d = r[2] + r[3];
+        if (a_d > -INFINITY) mdq = fmax(mdq, r[2]);
+        m = fmax(ld, a_d);
+        ld = (m == -INFINITY) ? -INFINITY : m + log(exp(ld - m) + exp(a_d - m));
+        const double a_z = omt * r[0] + tau * r[2] + r[4];
+        m = fmax(lz, a_z);
+        lz = (m == -INFINITY) ? -INFINITY : m + log(exp(lz - m) + exp(a_z - m));
+        const int fl = (int)r[7];
+        f |= fl;
+        if (fl & 2) {
+          lty = r[5];
+          ldy = r[6];
         }
       }
-      const double lse_t = lt_m == -INFINITY ? -INFINITY : lt_m + log(lt_s);
-      const double lse_d = ld_m == -INFINITY ? -INFINITY : ld_m + log(ld_s);
-      const double lse_z = lz_m == -INFINITY ? -INFINITY : lz_m + log(lz_s);
+    }
+    auto warp_lse = [&](double x) -> double {
+      double m = x;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (m == -INFINITY) return -(double)INFINITY;
+      double e = (x == -INFINITY) ? 0.0 : exp(x - m);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+      return m + log(e);
+    };
+    auto warp_max = [&](double x) -> double {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+      return x;
+    };
+    const double lse_t = warp_lse(lt), lse_d = warp_lse(ld), lse_z = warp_lse(lz);
+    const double mt = warp_max(mtq), md = warp_max(mdq);
+    const unsigned diffq = __ballot_sync(0xffffffffu, (f & 1) != 0);
+    const unsigned ownq = __ballot_sync(0xffffffffu, (f & 2) != 0);
+    const int owner = ownq ? __ffs(ownq) - 1 : 0;
+    const double lt_y0 = __shfl_sync(0xffffffffu, lty, owner);
+    const double ld_y0 = __shfl_sync(0xffffffffu, ldy, owner);
+    // ---- top-m overlap: rank every slice candidate against all others ----
+    int shared = 0;
+    if (pair) {
+      const int nc = in.P * M;
+      const size_t lo = ((size_t)b * G + j) * 2 * M;
+      for (int r = 0; r < 2; ++r) {  // 0: target, 1: draft
+        for (int c = lane; c < ((nc + 31) & ~31); c += 32) {
+          const bool val = c < nc;
+          const int q = val ? c / M : 0, i = val ? c - (c / M) * M : 0;
+          const int id = val ? in.topi[q * in.topi_stride + lo + r * M + i] : -1;
+          const double v = val && id >= 0 ? in.topv[q * in.topv_stride + lo + r * M + i] : 0.0;
+          int rank = 0;
+          if (id >= 0) {
+            for (int qq = 0; qq < in.P; ++qq) {
+              if (qq == q) {
+                rank += i;  // own list is sorted: its first i entries beat it
+                continue;
+              }
+              const int32_t *ti = in.topi + qq * in.topi_stride + lo + r * M;
+              const double *tv = in.topv + qq * in.topv_stride + lo + r * M;
+              for (int ii = 0; ii < M; ++ii) {
+                const int id2 = ti[ii];
+                if (id2 < 0) break;
+                const double v2 = tv[ii];
+                if (!(v2 > v || (v2 == v && id2 < id))) break;  // sorted: no later entry beats it
+                ++rank;
+              }
+            }
+          }
+          const bool top = id >= 0 && rank < M;
+          if (r == 0) {
+            if (top) tset[warp][rank] = id;
+          } else {
+            __syncwarp();
+            bool hit = false;
+            if (top)
+              for (int k = 0; k < M; ++k) hit |= tset[warp][k] == id;
+            shared += __popc(__ballot_sync(0xffffffffu, hit));
+          }
+        }
+        if (r == 0) {
+          // fewer than M valid candidates: the rest of the set stays unmatched
+          __syncwarp();
+        }
+      }
+    }
+    if (lane == 0) {
+      int err = 0, key = 0, kind = DSDV_EFF_TARGET, near = 0, accepted = 0;
+      double lt_y = lt_y0, ld_y = ld_y0;
       PosEval ev;
       ev.mt = mt;
       ev.lst = lse_t - mt;
@@ -129,25 +174,13 @@ __global__ void __launch_bounds__(128)
       ev.lsd = pair ? lse_d - md : 0.0;
       ev.lsz = 0.0;
       ev.h_t = ev.h_d = ev.p_t_y = ev.p_d_y = ev.nm = ev.p_eff = ev.a = ev.u = 0.0;
-      // distribution invariants: every row has mass
       if (!(lse_t > -INFINITY && isfinite(lse_t))) err = DSDV_E_INVARIANT;
       if (pair) {
         if (!(lse_d > -INFINITY && isfinite(lse_d)) && !err) err = DSDV_E_INVARIANT;
         const int y = tokens[(size_t)b * G + j];
-        if (!(own && y >= 0 && y < p.V) && !err) err = DSDV_E_INVARIANT;  // check_token_in_vocab
-        if (!own) lt_y = ld_y = -INFINITY;
-        // ---- top-m overlap (norm_match, verifier.cpp:119-134) ----
-        int tt[kMaxTopM], td[kMaxTopM];
-        const size_t lo = ((size_t)b * G + j) * 2 * M;
-        merge_top(in, lo, top_stride_p, M, tt);
-        merge_top(in, lo + M, top_stride_p, M, td);
-        int shared = 0;
-        for (int x = 0; x < M; ++x) {
-          if (td[x] < 0) continue;
-          for (int w = 0; w < M; ++w) shared += (tt[w] == td[x]) ? 1 : 0;
-        }
+        if (!(ownq && y >= 0 && y < p.V) && !err) err = DSDV_E_INVARIANT;  // check_token_in_vocab
+        if (!ownq) lt_y = ld_y = -INFINITY;
         ev.nm = (double)shared / (double)M;
-        // ---- is_key (verifier.cpp:136-159) ----
         ev.h_t = (lt_y == -INFINITY) ? INFINITY : lse_t - lt_y;
         ev.h_d = (ld_y == -INFINITY) ? INFINITY : lse_d - ld_y;
         ev.p_t_y = exp(lt_y - lse_t);
@@ -164,8 +197,7 @@ __global__ void __launch_bounds__(128)
             fabs(ev.h_d / ev.h_t - p.ratio_limit) < el * fmax(1.0, p.ratio_limit))
           near = 1;
         if (fabs(gap - p.gap_limit) < el * fmax(1.0, p.gap_limit)) near = 1;
-        // ---- effective distribution and accept_prob (:188-196, :231-237) ----
-        if (key || p.tau == 0.0 || diff == 0)
+        if (key || p.tau == 0.0 || diffq == 0)
           kind = DSDV_EFF_TARGET;
         else if (p.tau == 1.0)
           kind = DSDV_EFF_DRAFT;
@@ -200,62 +232,83 @@ __global__ void __launch_bounds__(128)
         if (o.p_effective_y) o.p_effective_y[pos] = ev.p_eff;
         if (o.uniform) o.uniform[pos] = ev.u;
       }
-      // global record of this row for the extra draw (dsdv_shard_sample)
-      double *r = o.records + ((size_t)b * G1 + j) * kRecordWords;
-      r[kRecMt] = ev.mt;
-      r[kRecLst] = ev.lst;
-      r[kRecMd] = ev.md;
-      r[kRecLsd] = ev.lsd;
-      r[kRecLsz] = ev.lsz;
-      r[kRecFlags] = (double)(kind | (err << 8) | (key << 16));
+      double *rr = o.records + ((size_t)b * G1 + j) * kRecordWords;
+      rr[kRecMt] = ev.mt;
+      rr[kRecLst] = ev.lst;
+      rr[kRecMd] = ev.md;
+      rr[kRecLsd] = ev.lsd;
+      rr[kRecLsz] = ev.lsz;
+      rr[kRecFlags] = (double)(kind | (err << 8) | (key << 16));
+      summ[j] = PosSummary{err, key, kind, near, accepted};
     }
-    // ---- first rejection or error, left to right (verifier.cpp:223-250) ----
-    const unsigned stop = __ballot_sync(0xffffffffu, active && j < G && (err || !accepted));
-    const unsigned upto = stop ? ((__ffs(stop) - 1) < 31 ? (1u << (__ffs(stop))) - 1u : 0xffffffffu)
-                               : 0xffffffffu;  // evaluated lanes: up to and incl. the stop
-    if (k == G) {
-      keys += __popc(__ballot_sync(0xffffffffu, active && j < G && key) & upto);
-      nears += __popc(__ballot_sync(0xffffffffu, active && j < G && near) & upto);
-      if (stop) {
-        const int src = __ffs(stop) - 1;
-        k = j0 + src;
-        stop_err = __shfl_sync(0xffffffffu, err, src);
-        stop_kind = __shfl_sync(0xffffffffu, kind, src);
-      }
-    }
-    __syncwarp();
   }
-  if (lane == 0) {
-    int st = DSDV_OK, pos = -1;
-    double u = 0.0;
-    if (k < G) {
-      if (stop_err) {
-        st = stop_err;
-      } else if (stop_kind == DSDV_EFF_DRAFT) {
-        st = DSDV_E_EMPTY_RESIDUAL;  // residual of P_d against itself (verifier.cpp:209-211)
-      } else {
-        pos = k;
-        u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b, (uint32_t)(G + k + 1));
-      }
-    } else {
-      const double *rb = o.records + ((size_t)b * G1 + G) * kRecordWords;
-      const int berr = ((int)rb[kRecFlags] >> 8) & 0xff;
-      if (berr) {
-        st = berr;
+  __syncthreads();
+  // ---- first rejection or error, left to right (verifier.cpp:223-250) ----
+  if (warp == 0) {
+    const bool act = lane < G;
+    const PosSummary sj = act ? summ[lane] : PosSummary{0, 0, 0, 0, 1};
+    const unsigned stop = __ballot_sync(0xffffffffu, act && (sj.err || !sj.accepted));
+    const int k = stop ? __ffs(stop) - 1 : G;
+    const unsigned upto = (k >= 31) ? 0xffffffffu : ((1u << (k + 1)) - 1u);
+    const int keys = __popc(__ballot_sync(0xffffffffu, act && sj.key) & upto);
+    const int nears = __popc(__ballot_sync(0xffffffffu, act && sj.near) & upto);
+    if (lane == 0) {
+      int st = DSDV_OK, pos = -1;
+      double u = 0.0;
+      if (k < G) {
+        if (summ[k].err) {
+          st = summ[k].err;
+        } else if (summ[k].kind == DSDV_EFF_DRAFT) {
+          st = DSDV_E_EMPTY_RESIDUAL;  // residual of P_d against itself (verifier.cpp:209-211)
+        } else {
+          pos = k;
+          u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b,
+                                  (uint32_t)(G + k + 1));
+        }
+      } else if (summ[G].err) {
+        st = summ[G].err;
       } else {
         pos = G;
         u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b, (uint32_t)(2 * G));
       }
+      o.accepted_count[b] = k;
+      o.key_count[b] = keys;
+      o.extra_source[b] = (k < G) ? DSDV_EXTRA_RESIDUAL : DSDV_EXTRA_BONUS;
+      o.extra_token[b] = -1;
+      o.status[b] = st;
+      o.near_threshold[b] = nears;
+      position[b] = pos;
+      uniform[b] = u;
+      s_pos = pos;
+      if (pos >= 0) {
+        const double *r = o.records + ((size_t)b * G1 + pos) * kRecordWords;
+        const int kind = (int)r[kRecFlags] & 0xff;
+        PosEval ev;
+        ev.mt = r[kRecMt];
+        ev.lst = r[kRecLst];
+        ev.md = r[kRecMd];
+        ev.lsd = r[kRecLsd];
+        ev.lsz = r[kRecLsz];
+        set_weigher(wf, pos == G ? kWeightPlain
+                                 : (kind == DSDV_EFF_SOFTENED ? kWeightResSoft : kWeightResTarget),
+                    ev, omt, tau);
+      }
     }
-    o.accepted_count[b] = k;
-    o.key_count[b] = keys;
-    o.extra_source[b] = (k < G) ? DSDV_EXTRA_RESIDUAL : DSDV_EXTRA_BONUS;
-    o.extra_token[b] = -1;
-    o.status[b] = st;
-    o.near_threshold[b] = nears;
-    position[b] = pos;
-    uniform[b] = u;
   }
+  __syncthreads();
+  // ---- this slice's mass of the extra-draw row (fused MASS step) ----
+  const int pos = s_pos;
+  if (pos < 0) {
+    if (threadIdx.x == 0) mass_out[b] = 0.0;
+    return;
+  }
+  if (threadIdx.x >= kConsumerThreads) return;
+  const In *rt = target + ((size_t)b * G1 + pos) * (size_t)p.stride;
+  const In *rd = draft + ((size_t)b * G + (pos < G ? pos : 0)) * (size_t)p.stride;
+  int near = 0;
+  cdf_sample<In, Acc>(rt, rd, wf, p.vocab_local, 0.0, p.eps_u, &samp, threadIdx.x, &near, -1.0,
+                      tiles ? tiles + (size_t)b * (kMaxTiles + 2) : nullptr);
+  if (threadIdx.x == 0) mass_out[b] = samp.W;
 }
 
 // Extra draw over a sharded row. MASS: the slice's weight total. RESOLVE: the
@@ -268,7 +321,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
                         const double *__restrict__ records, const int32_t *__restrict__ position,
                         const double *__restrict__ uniform, const double *__restrict__ masses,
                         double *__restrict__ mass_out, int32_t *__restrict__ token_out,
-                        int32_t *__restrict__ status) {
+                        int32_t *__restrict__ status, const double *__restrict__ tiles) {
   using Acc = typename InTraits<In>::Acc;
   __shared__ SampleShared samp;
   __shared__ Weigher<Acc> wf;
@@ -338,8 +391,9 @@ __global__ void __launch_bounds__(kConsumerThreads)
   const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
   const In *rd = draft + ((size_t)b * G + (j < G ? j : 0)) * (size_t)p.stride;
   int near = 0;
-  const int idx = cdf_sample<In, Acc>(rt, rd, wf, p.vocab_local, 0.0, p.eps_u, &samp, tid, &near,
-                                      mode == 1 ? t_local : -1.0);
+  const int idx = cdf_sample<In, Acc>(
+      rt, rd, wf, p.vocab_local, 0.0, p.eps_u, &samp, tid, &near, mode == 1 ? t_local : -1.0,
+      nullptr, (mode == 1 && tiles) ? tiles + (size_t)b * (kMaxTiles + 2) : nullptr);
   if (tid == 0) {
     if (mode == 0)
       mass_out[b] = samp.W;
@@ -348,15 +402,25 @@ __global__ void __launch_bounds__(kConsumerThreads)
   }
 }
 
+template <class In>
 cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const double *topv,
-                               const int32_t *topi, int P, const int32_t *tokens, const DevOut &o,
-                               int32_t *position, double *uniform, cudaStream_t stream) {
-  if (P < 1 || P > kMaxShards) return cudaErrorInvalidValue;
-  MergeIn in{rec, topv, topi, P};
-  const int warps_per_block = 4;
-  const int grid = (p.B + warps_per_block - 1) / warps_per_block;
-  shard_merge_kernel<<<grid, 32 * warps_per_block, 0, stream>>>(p, in, tokens, o, position,
-                                                                  uniform);
+                               const int32_t *topi, int P, size_t rank_bytes, const void *draft,
+                               const void *target, const int32_t *tokens, const DevOut &o,
+                               int32_t *position, double *uniform, double *mass_out,
+                               double *tiles, cudaStream_t stream) {
+  if (P < 1 || P > kMaxShards || p.gamma > 31) return cudaErrorInvalidValue;
+  const int G1 = p.gamma + 1;
+  MergeIn in{rec, topv, topi, P, (size_t)p.B * G1 * kRecordWords,
+             (size_t)p.B * p.gamma * 2 * p.top_m, (size_t)p.B * p.gamma * 2 * p.top_m};
+  if (rank_bytes) {
+    if (rank_bytes % 8) return cudaErrorInvalidValue;
+    in.rec_stride = in.topv_stride = rank_bytes / 8;
+    in.topi_stride = rank_bytes / 4;
+  }
+  const int threads = 32 * G1 > kConsumerThreads ? 32 * G1 : kConsumerThreads;
+  shard_merge_kernel<In><<<p.B, threads, 0, stream>>>(p, in, (const In *)draft,
+                                                      (const In *)target, tokens, o, position,
+                                                      uniform, mass_out, tiles);
   return cudaGetLastError();
 }
 
@@ -365,25 +429,36 @@ cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nran
                                 const void *draft, const void *target, const double *records,
                                 const int32_t *position, const double *uniform,
                                 const double *masses, double *mass_out, int32_t *token_out,
-                                int32_t *status, cudaStream_t stream) {
+                                int32_t *status, const double *tiles, cudaStream_t stream) {
   shard_sample_kernel<In><<<p.B, kConsumerThreads, 0, stream>>>(
       p, mode, rank, nranks, (const In *)draft, (const In *)target, records, position, uniform,
-      masses, mass_out, token_out, status);
+      masses, mass_out, token_out, status, tiles);
   return cudaGetLastError();
 }
+
+#define DSDV_MERGE_INST(T)                                                                   \
+  template cudaError_t launch_shard_merge<T>(const DevParams &, const double *, const double *,  \
+                                             const int32_t *, int, size_t, const void *,        \
+                                             const void *, const int32_t *, const DevOut &,     \
+                                             int32_t *, double *, double *, double *, cudaStream_t);
+DSDV_MERGE_INST(__nv_bfloat16)
+DSDV_MERGE_INST(float)
+DSDV_MERGE_INST(double)
+#undef DSDV_MERGE_INST
 
 template cudaError_t launch_shard_sample<__nv_bfloat16>(const DevParams &, int, int, int,
                                                         const void *, const void *, const double *,
                                                         const int32_t *, const double *,
                                                         const double *, double *, int32_t *,
-                                                        int32_t *, cudaStream_t);
+                                                        int32_t *, const double *, cudaStream_t);
 template cudaError_t launch_shard_sample<float>(const DevParams &, int, int, int, const void *,
                                                 const void *, const double *, const int32_t *,
                                                 const double *, const double *, double *,
-                                                int32_t *, int32_t *, cudaStream_t);
+                                                int32_t *, int32_t *, const double *, cudaStream_t);
 template cudaError_t launch_shard_sample<double>(const DevParams &, int, int, int, const void *,
                                                  const void *, const double *, const int32_t *,
                                                  const double *, const double *, double *,
-                                                 int32_t *, int32_t *, cudaStream_t);
+                                                 int32_t *, int32_t *, const double *,
+                                                 cudaStream_t);
 
 }  // namespace dsdv

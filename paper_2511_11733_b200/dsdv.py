@@ -83,10 +83,10 @@ def _load() -> C.CDLL:
         "dsdv_synth_logits": (st, [vp, C.POINTER(_Params), C.c_uint64, vp, vp, vp]),
         "dsdv_launch_count": (C.c_uint64, [vp]),
         "dsdv_shard_stats": (st, [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp]),
-        "dsdv_shard_merge": (st, [vp, C.POINTER(_Params), C.c_int32, vp, vp, vp, vp,
-                                  C.POINTER(_Outputs), vp, vp, vp]),
+        "dsdv_shard_merge": (st, [vp, C.POINTER(_Params), C.c_int32, vp, vp, vp, C.c_uint64, vp,
+                                  vp, vp, C.POINTER(_Outputs), vp, vp, vp, vp, vp]),
         "dsdv_shard_sample": (st, [vp, C.POINTER(_Params), C.c_int32, C.c_int32, C.c_int32, vp,
-                                   vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+                                   vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "dsdv_mix_rows": (st, [vp, C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp, vp]),
         "dsdv_spin": (st, [vp, C.c_uint64, vp]),
     }
