@@ -1490,7 +1490,7 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
   const int G1 = p.gamma + 1;
   int stage = 0;
   uint32_t phase = 0;
-  int n = 0;
+  int n = 0, next = -1;
   bool exhausted = false;
   for (;;) {
     // sample requests first: their rows are still L2-resident
@@ -1513,8 +1513,12 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       continue;
     }
     if (!exhausted) {
-      const int item = (int)atomicAdd(s.ticket, 1u);
+      const int item = next >= 0 ? next : (int)atomicAdd(s.ticket, 1u);
+      next = -1;
       if (item < p.n_items) {
+        // claim the following item now: the global atomic's round trip
+        // overlaps this item's copies instead of delaying the next item
+        next = (int)atomicAdd(s.ticket, 1u);
         const int j = item / p.B, b = item - j * p.B;  // position-major order
         const bool pair = j < p.gamma;
         const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
