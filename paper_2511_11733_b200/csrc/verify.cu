@@ -1462,7 +1462,7 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
   constexpr int CH = kRowBytes / (int)sizeof(In);
   for (int c = 0; c < n_chunks; ++c) {
     TR_START(tw);
-    mbar_wait(&sm.empty[stage], phase ^ 1);
+    mbar_wait_spin(&sm.empty[stage], phase ^ 1);
     TR_ADD(tr, kTrProdWaitEmpty, tw);
     StageMeta m;
     m.item = item;
