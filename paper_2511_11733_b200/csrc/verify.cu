@@ -562,6 +562,16 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     TR_START(tw);
     mbar_wait(&sm.full[stage], phase);
     TR_ADD(trl, kTrComputeWaitFull, tw);
+#ifdef DSDV_TIMELINE
+    if (trl && warp == 0 && blockIdx.x == 0) {
+      unsigned long long *tl = tr + 512 * kTraceWords;
+      const unsigned q = (unsigned)tl[4094];
+      if (q < 1000) {
+        tl[q * 4 + 1] = clock64();
+        tl[q * 4 + 2] = clock64() - tw;
+      }
+    }
+#endif
     const StageMeta md = sm.meta[stage];
     if (md.item < 0) {
       // end of stream: one terminating slot per epilogue warp
@@ -609,6 +619,13 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
                        reinterpret_cast<double *>(sm.slot[s].area), p, tid, warp, lane);
     }
     TR_ADD(trl, kind == kRegular ? kTrComputeFold : kTrComputeSample, tf);
+#ifdef DSDV_TIMELINE
+    if (trl && warp == 0 && blockIdx.x == 0) {
+      unsigned long long *tl = tr + 512 * kTraceWords;
+      const unsigned q = (unsigned)tl[4094]++;
+      if (q < 1000) tl[q * 4 + 3] = clock64();
+    }
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[stage]);
     if (++stage == Smem<Acc>::kStages) {
@@ -1473,6 +1490,13 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
     const int rem = nlocal - c * CH;
     const int elems = rem < CH ? rem : CH;
     const uint32_t bytes = ((uint32_t)(elems * (int)sizeof(In)) + 15u) & ~15u;
+#ifdef DSDV_TIMELINE
+    if (tr && blockIdx.x == 0) {
+      unsigned long long *tl = tr + 512 * kTraceWords;
+      const unsigned q = (unsigned)tl[4095]++;
+      if (q < 1000) tl[q * 4 + 0] = clock64();
+    }
+#endif
     mbar_arrive_expect_tx(&sm.full[stage], two ? 2u * bytes : bytes);
     bulk_g2s(sm.ring[stage][1], rt + (size_t)c * CH, bytes, &sm.full[stage]);
     if (two) bulk_g2s(sm.ring[stage][0], rd + (size_t)c * CH, bytes, &sm.full[stage]);
