@@ -40,6 +40,16 @@ def test_c2_vocab_bf16(verifier, oracle):
     _check(rep)
 
 
+@pytest.mark.parametrize("tau", [0.1, 0.3, 0.5])
+def test_c3_shape_fp32(verifier, oracle, tau):
+    """C3 per sequence: V=151936 (Qwen), gamma=16, fp32, tau in the C3 sweep."""
+    crit = _crit(oracle, 2.5, 0.15, 0.4, 10)
+    d, t, tok, gpu, _ = run_gpu_window(verifier, torch.float32, 4, 16, 151936, tau, crit,
+                                       seed=3, oracle=oracle)
+    rep = compare_window(oracle, d, t, tok, gpu, tau, crit, seed=3, window=0)
+    _check(rep)
+
+
 @pytest.mark.parametrize("tau", [0.0, 0.5, 1.0])
 def test_tau_endpoints_and_mid(verifier, oracle, tau):
     d, t, tok, gpu, _ = run_gpu_window(verifier, torch.float32, 12, 6, 5000, tau,
