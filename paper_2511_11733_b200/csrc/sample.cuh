@@ -232,11 +232,14 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
         if ((t + k) < t1 && base < n) {
           Acc w[VEC];
           vec_weights<In, Acc>(rt[k], rd[k], base, n, wf, w);
+          // lane sum in the accumulation type, one conversion per vector
+          Acc lv = Acc(0);
 #pragma unroll
           for (int e = 0; e < VEC; ++e) {
             if (w[e] > Acc(0)) last = base + e;
-            ls[k] += (double)w[e];
+            lv += w[e];
           }
+          ls[k] += (double)lv;
         }
       }
     }
