@@ -245,6 +245,9 @@ class RefOracle:
         L.ref_accept_prob.argtypes = [_dp, _dp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.ref_residual.argtypes = [_dp, _dp, C.c_int, _dp]
         L.ref_sample_with_uniform.argtypes = [_dp, C.c_int, C.c_double, C.POINTER(C.c_int)]
+        L.ref_enumerate_first.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double,
+                                          C.c_double, C.c_double, C.c_int, _dp,
+                                          C.POINTER(C.c_double)]
         L.ref_softmax.argtypes = [_dp, C.c_int, _dp]
         L.ref_seeded_uniform.argtypes = [C.c_uint64, C.c_int]
         L.ref_seeded_uniform.restype = C.c_double
@@ -356,6 +359,19 @@ class RefOracle:
                                     crit.gap_limit, crit.overlap_floor, crit.top_m,
                                     self._a(uniforms), nthreads or os.cpu_count(), k, e, s)
         return k, e, s
+
+    def enumerate_first(self, pd, pt, gamma, tau, crit):
+        """Exact distribution of the first committed token and E[accepted] of
+        one round (enumerate_output_distribution / expected_accepted_count)."""
+        pd, pt = self._a(pd), self._a(pt)
+        out = np.zeros(pd.size, np.float64)
+        ek = C.c_double()
+        st = self.L.ref_enumerate_first(pd, pt, pd.size, gamma, tau, crit.ratio_limit,
+                                        crit.gap_limit, crit.overlap_floor, crit.top_m, out,
+                                        C.byref(ek))
+        if st != 0:
+            raise RuntimeError(f"ref_enumerate_first failed with status {-st}")
+        return out, ek.value
 
     def generate_iid(self, pd, pt, gamma, tau, crit, max_new, seed):
         pd, pt = self._a(pd), self._a(pt)

@@ -311,4 +311,24 @@ int ref_generate_iid(const double *pd, const double *pt, int V, int gamma, doubl
   }
 }
 
+// ---- exact enumeration (enumerate.cpp) for the GPU statistical checks ----
+// Distribution of the first committed token and E[accepted] of one round,
+// categorical-iid models.
+int ref_enumerate_first(const double *pd, const double *pt, int V, int gamma, double tau,
+                        double r, double g, double o, int m, double *out, double *expected_k) {
+  try {
+    const dsd::TokenModel draft = dsd::TokenModel::categorical(dist(pd, V));
+    const dsd::TokenModel target = dsd::TokenModel::categorical(dist(pt, V));
+    const dsd::VerifyParams params{gamma, tau, crit_of(r, g, o, m)};
+    const dsd::SequenceDistribution d =
+        dsd::enumerate_output_distribution(draft, target, dsd::Context{}, 1, params);
+    for (int i = 0; i < V; ++i) out[i] = 0.0;
+    for (const auto &kv : d) out[kv.first.at(0)] += kv.second;
+    *expected_k = dsd::expected_accepted_count(draft, target, dsd::Context{}, params);
+    return 0;
+  } catch (...) {
+    return -code_of(std::current_exception());
+  }
+}
+
 }  // extern "C"
