@@ -39,6 +39,21 @@ def comm_reduction_ratio(tokens: float, n_nodes: int, t0: float, t1: float) -> f
     return sync_cost(n_nodes, t1) * (tokens - 1.0) / (tokens * (t0 + sync_cost(n_nodes, t1)))
 
 
+def expected_speedup(rho: float, mean_accepted: float, n_nodes: int, t0: float,
+                     t1: float) -> float:
+    """latency.cpp:88-95: (t0 + sync) / (t0 / rho + sync / mean_accepted)."""
+    sync = sync_cost(n_nodes, t1)
+    return (t0 + sync) / (t0 / rho + sync / mean_accepted)
+
+
+def analytic_speedup(rho: float, mean_accepted: float, n_nodes: int, t0: float,
+                     t1: float) -> float:
+    """commands.cpp:64-71: the closed form, or 0 for degenerate runs."""
+    if rho > 0.0 and mean_accepted >= 1.0:
+        return expected_speedup(rho, mean_accepted, n_nodes, t0, t1)
+    return 0.0
+
+
 # ---- the reference's pipeline with constant link latency ------------------
 @dataclass
 class Unit:

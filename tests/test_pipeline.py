@@ -59,3 +59,11 @@ def test_device_emulation_tracks_the_model():
     assert abs(t_std - des_std) / des_std < 0.1
     assert abs(t_dsd - des_dsd) / des_dsd < 0.1
     assert abs((1 - t_dsd / t_std) - (1 - des_dsd / des_std)) < 0.03
+
+
+def test_expected_speedup_known_answers():
+    # latency.cpp:88-95 at kReference {N=4, t0=1, t1=5}: rho=1, k=1 -> 1 (no gain);
+    # amortisation grows with the accepted span
+    assert abs(pl.expected_speedup(1.0, 1.0, 4, 1.0, 5.0) - 1.0) < 1e-12
+    assert pl.expected_speedup(0.5, 4.0, 4, 1.0, 5.0) > pl.expected_speedup(0.5, 2.0, 4, 1.0, 5.0)
+    assert pl.analytic_speedup(0.0, 2.0, 4, 1.0, 5.0) == 0.0
