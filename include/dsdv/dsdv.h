@@ -167,6 +167,12 @@ dsdv_status dsdv_sample_extra(dsdv_ctx *ctx, const dsdv_params *params,
  * with the Philox draft slot j (philox.h). */
 dsdv_status dsdv_draft_sample(dsdv_ctx *ctx, const dsdv_params *params,
                               const void *draft_logits, int32_t *draft_tokens, void *stream);
+/* The same under a sampling temperature (temperature_scale,
+ * distribution.cpp:65-97): T = 1 identity, T = 0 the argmax with the lowest id
+ * on ties, else softmax(l / T). */
+dsdv_status dsdv_draft_sample_temperature(dsdv_ctx *ctx, const dsdv_params *params,
+                                          double temperature, const void *draft_logits,
+                                          int32_t *draft_tokens, void *stream);
 
 /* Whole-row mixtures of two fp64 probability vectors of length vocab (the
  * drop-in API's soften and residual_distribution, verifier.cpp:161-186 and

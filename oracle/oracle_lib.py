@@ -245,6 +245,7 @@ class RefOracle:
         L.ref_accept_prob.argtypes = [_dp, _dp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.ref_residual.argtypes = [_dp, _dp, C.c_int, _dp]
         L.ref_sample_with_uniform.argtypes = [_dp, C.c_int, C.c_double, C.POINTER(C.c_int)]
+        L.ref_temperature_scale.argtypes = [_dp, C.c_int, C.c_double, _dp]
         L.ref_enumerate_first.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double,
                                           C.c_double, C.c_double, C.c_int, _dp,
                                           C.POINTER(C.c_double)]
@@ -359,6 +360,14 @@ class RefOracle:
                                     crit.gap_limit, crit.overlap_floor, crit.top_m,
                                     self._a(uniforms), nthreads or os.cpu_count(), k, e, s)
         return k, e, s
+
+    def temperature_scale(self, p, T):
+        p = self._a(p)
+        out = np.zeros(p.size, np.float64)
+        st = self.L.ref_temperature_scale(p, p.size, T, out)
+        if st != 0:
+            raise RuntimeError(f"ref_temperature_scale failed with status {-st}")
+        return out
 
     def enumerate_first(self, pd, pt, gamma, tau, crit):
         """Exact distribution of the first committed token and E[accepted] of

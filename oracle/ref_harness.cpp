@@ -311,6 +311,17 @@ int ref_generate_iid(const double *pd, const double *pt, int V, int gamma, doubl
   }
 }
 
+// ---- temperature_scale (distribution.cpp:65-97) ----
+int ref_temperature_scale(const double *p, int V, double T, double *out) {
+  try {
+    const dsd::Distribution d = dsd::temperature_scale(dist(p, V), T);
+    std::memcpy(out, d.probs().data(), sizeof(double) * (size_t)V);
+    return 0;
+  } catch (...) {
+    return -code_of(std::current_exception());
+  }
+}
+
 // ---- exact enumeration (enumerate.cpp) for the GPU statistical checks ----
 // Distribution of the first committed token and E[accepted] of one round,
 // categorical-iid models.

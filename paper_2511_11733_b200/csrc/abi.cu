@@ -21,7 +21,8 @@ cudaError_t launch_sample_extra(const DevParams &, const void *, const void *, c
                                 const int32_t *, const double *, int32_t *, int32_t *,
                                 cudaStream_t);
 template <class In>
-cudaError_t launch_draft_sample(const DevParams &, const void *, int32_t *, cudaStream_t);
+cudaError_t launch_draft_sample(const DevParams &, const void *, int32_t *, double,
+                                cudaStream_t);
 template <class In>
 cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const double *topv,
                                const int32_t *topi, int P, size_t rank_bytes, const void *draft,
@@ -536,7 +537,16 @@ dsdv_status dsdv_mix_rows(dsdv_ctx *ctx, int32_t kind, int32_t vocab, const doub
 
 dsdv_status dsdv_draft_sample(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,
                               int32_t *draft_tokens, void *stream) {
+  return dsdv_draft_sample_temperature(ctx, params, 1.0, draft_logits, draft_tokens, stream);
+}
+
+dsdv_status dsdv_draft_sample_temperature(dsdv_ctx *ctx, const dsdv_params *params,
+                                          double temperature, const void *draft_logits,
+                                          int32_t *draft_tokens, void *stream) {
   if (!ctx) return DSDV_E_INVARIANT;
+  if (!(std::isfinite(temperature) && temperature >= 0.0))
+    return fail(ctx, DSDV_E_INVARIANT, "temperature must be a finite non-negative real, got %s",
+                std::to_string(temperature).c_str());
   DevParams d;
   dsdv_status st = build_params(ctx, params, d);
   if (st != DSDV_OK) return st;
@@ -548,14 +558,16 @@ dsdv_status dsdv_draft_sample(dsdv_ctx *ctx, const dsdv_params *params, const vo
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
   switch (params->dtype) {
     case DSDV_DTYPE_BF16:
-      e = dsdv::launch_draft_sample<__nv_bfloat16>(d, draft_logits, draft_tokens,
+      e = dsdv::launch_draft_sample<__nv_bfloat16>(d, draft_logits, draft_tokens, temperature,
                                                    (cudaStream_t)stream);
       break;
     case DSDV_DTYPE_F32:
-      e = dsdv::launch_draft_sample<float>(d, draft_logits, draft_tokens, (cudaStream_t)stream);
+      e = dsdv::launch_draft_sample<float>(d, draft_logits, draft_tokens, temperature,
+                                           (cudaStream_t)stream);
       break;
     default:
-      e = dsdv::launch_draft_sample<double>(d, draft_logits, draft_tokens, (cudaStream_t)stream);
+      e = dsdv::launch_draft_sample<double>(d, draft_logits, draft_tokens, temperature,
+                                            (cudaStream_t)stream);
       break;
   }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "draft_sample launch");

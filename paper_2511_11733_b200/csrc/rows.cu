@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
 template <class In>
 __global__ void __launch_bounds__(kConsumerThreads)
     draft_sample_kernel(const __grid_constant__ DevParams p, const In *__restrict__ draft,
-                        int32_t *__restrict__ tokens) {
+                        int32_t *__restrict__ tokens, double temperature) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   __shared__ RowsSmem sm;
@@ -94,51 +94,92 @@ __global__ void __launch_bounds__(kConsumerThreads)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const In *rd = draft + (size_t)row * p.stride;
   const Acc ni = neg_inf<Acc>();
+  // temperature_scale (distribution.cpp:65-97): T = 1 identity, T = 0 one-hot
+  // at the argmax (lowest id on ties), else p^(1/T) = softmax(l / T)
+  const bool argmax = temperature == 0.0;
+  const Acc it = (argmax || temperature == 1.0) ? Acc(1) : Acc(1.0 / temperature);
+  const Acc itL = it * log2e<Acc>();
   Acc m = ni, s = Acc(0);
+  int am = 0x7fffffff;  // argmax id (T = 0)
   const int nvec = (p.vocab_local + VEC - 1) / VEC;
   for (int q = tid; q < nvec; q += kConsumerThreads) {
     Acc v[VEC];
     unpack(ldg128(rd + (size_t)q * VEC), v, (In *)nullptr);
     Acc cm = ni;
+    int ci = 0x7fffffff;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       if (q * VEC + e >= p.vocab_local) v[e] = ni;
-      cm = v[e] > cm ? v[e] : cm;
+      if (v[e] > cm) {  // strict: the lowest id keeps ties
+        cm = v[e];
+        ci = q * VEC + e;
+      }
     }
+    if (cm > m || (cm == m && ci < am)) am = ci;
     Acc cs = Acc(0);
     if (cm != ni) {
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) cs += fast_exp2((v[e] - cm) * log2e<Acc>());
+      for (int e = 0; e < VEC; ++e) cs += fast_exp2((v[e] - cm) * itL);
     }
-    merge_ms(m, s, cm, cs);
+    // running (max, sum of exp((v - max) / T))
+    if (cm > m) {
+      s = (m == ni ? Acc(0) : s * fast_exp2((m - cm) * itL)) + cs;
+      m = cm;
+    } else if (cm != ni) {
+      s += cs * fast_exp2((cm - m) * itL);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const Acc m2 = __shfl_xor_sync(0xffffffffu, m, o);
     const Acc s2 = __shfl_xor_sync(0xffffffffu, s, o);
-    merge_ms(m, s, m2, s2);
+    const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
+    if (m2 > m || (m2 == m && a2 < am)) am = a2;
+    if (m2 > m) {
+      s = (m == ni ? Acc(0) : s * fast_exp2((m - m2) * itL)) + s2;
+      m = m2;
+    } else if (m2 != ni) {
+      s += s2 * fast_exp2((m2 - m) * itL);
+    }
   }
+  __shared__ int red_a[kConsumerWarps];
   if (lane == 0) {
     sm.red_m[warp] = (double)m;
     sm.red_s[warp] = (double)s;
+    red_a[warp] = am;
   }
   __syncthreads();
+  if (argmax) {
+    if (tid == 0) {
+      double M = sm.red_m[0];
+      int A = red_a[0];
+      for (int w = 1; w < kConsumerWarps; ++w)
+        if (sm.red_m[w] > M || (sm.red_m[w] == M && red_a[w] < A)) {
+          M = sm.red_m[w];
+          A = red_a[w];
+        }
+      tokens[row] = (M == -INFINITY || A == 0x7fffffff) ? -1 : p.vocab_offset + A;
+    }
+    return;
+  }
   if (tid == 0) {
     double M = sm.red_m[0], S = sm.red_s[0];
     for (int w = 1; w < kConsumerWarps; ++w) {
       const double m2 = sm.red_m[w], s2 = sm.red_s[w];
       if (m2 == -INFINITY) continue;
       if (m2 > M) {
-        S = (M == -INFINITY ? 0.0 : S * exp(M - m2)) + s2;
+        S = (M == -INFINITY ? 0.0 : S * exp((M - m2) * (double)it)) + s2;
         M = m2;
       } else {
-        S += s2 * exp(m2 - M);
+        S += s2 * exp((m2 - M) * (double)it);
       }
     }
     PosEval ev;
-    ev.mt = M;
+    ev.mt = M;  // a row element: exact in Acc, so no rounding correction is scaled
     ev.lst = log(S);
     ev.md = ev.lsd = ev.lsz = 0.0;
     set_weigher(wf, kWeightPlain, ev, (double)p.omt_f, (double)p.tau_f);
+    wf.itemp = it;
+    wf.itL = (float)((double)it * kLog2e);
   }
   __syncthreads();
   const double u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b, (uint32_t)j);
@@ -235,9 +276,9 @@ cudaError_t launch_sample_extra(const DevParams &p, const void *draft, const voi
 
 template <class In>
 cudaError_t launch_draft_sample(const DevParams &p, const void *draft, int32_t *tokens,
-                                cudaStream_t stream) {
+                                double temperature, cudaStream_t stream) {
   draft_sample_kernel<In><<<p.B * p.gamma, kConsumerThreads, 0, stream>>>(p, (const In *)draft,
-                                                                          tokens);
+                                                                          tokens, temperature);
   return cudaGetLastError();
 }
 
@@ -314,7 +355,7 @@ cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, d
                                               const double *, const int32_t *, const double *,  \
                                               int32_t *, int32_t *, cudaStream_t);               \
   template cudaError_t launch_draft_sample<T>(const DevParams &, const void *, int32_t *,        \
-                                              cudaStream_t);
+                                              double, cudaStream_t);
 DSDV_INST(__nv_bfloat16)
 DSDV_INST(float)
 DSDV_INST(double)

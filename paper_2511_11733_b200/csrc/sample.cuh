@@ -48,9 +48,14 @@ struct Weigher {
   // fp32 packed path (weigh_vec): exponents in log2 units, constants split
   // hi/lo so that they stay exact relative to the (small) exponent
   float kt_hi, kt_lo, kd_hi, kd_lo, kz_hi, kz_lo, omtL, tauL;
+  // plain (bonus / draft) rows under a temperature: P(i) ~ exp((t_i - mt) / T)
+  // (temperature_scale, distribution.cpp:65-97); itemp = 1 / T, 1 otherwise
+  Acc itemp;
+  float itL;
 
   __device__ __forceinline__ Acc p_t(Acc t) const {
-    return fast_exp2(mul_rn(sub_rn(sub_rn(sub_rn(t, mt), ct_hi), ct_lo), log2e<Acc>()));
+    return fast_exp2(
+        mul_rn(sub_rn(sub_rn(mul_rn(sub_rn(t, mt), itemp), ct_hi), ct_lo), log2e<Acc>()));
   }
   __device__ __forceinline__ Acc operator()(Acc t, Acc d) const {
     if (kind == kWeightPlain) return p_t(t);
@@ -82,7 +87,7 @@ __device__ __forceinline__ void weigh_vec(const Weigher<float> &wf, const float 
     const f32x2 a2 = sub2(pk2(vt[e], vt[e + 1]), mt2);
     f32x2 r;
     if (wf.kind == kWeightPlain) {
-      const f32x2 xt = add2(fma2(a2, L2, kth), ktl);
+      const f32x2 xt = add2(fma2(a2, pk2(wf.itL, wf.itL), kth), ktl);
       r = pk2(fast_exp2(lo2(xt)), fast_exp2(hi2(xt)));
     } else {
       const f32x2 b2 = sub2(pk2(vd[e], vd[e + 1]), pk2(wf.md, wf.md));
@@ -143,6 +148,8 @@ __device__ __forceinline__ void set_weigher(Weigher<Acc> &wf, int kind, const Po
   split_hi_lo(-lz * kLog2e, wf.kz_hi, wf.kz_lo);
   wf.omtL = (float)(omt * kLog2e);
   wf.tauL = (float)(tau * kLog2e);
+  wf.itemp = Acc(1);
+  wf.itL = kLog2eF;
 }
 
 constexpr int kMaxTiles = 512;

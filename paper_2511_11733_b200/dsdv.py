@@ -89,6 +89,7 @@ def _load() -> C.CDLL:
                                    vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "dsdv_mix_rows": (st, [vp, C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp, vp]),
         "dsdv_spin": (st, [vp, C.c_uint64, vp]),
+        "dsdv_draft_sample_temperature": (st, [vp, C.POINTER(_Params), C.c_double, vp, vp, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -102,7 +103,7 @@ EXPORTED = ("dsdv_create", "dsdv_destroy", "dsdv_last_error", "dsdv_abi_version"
             "dsdv_verify", "dsdv_window_stats", "dsdv_sample_extra", "dsdv_draft_sample",
             "dsdv_sync", "dsdv_uniform", "dsdv_synth_logits", "dsdv_launch_count",
             "dsdv_shard_stats", "dsdv_shard_merge", "dsdv_shard_sample", "dsdv_mix_rows",
-            "dsdv_spin")
+            "dsdv_spin", "dsdv_draft_sample_temperature")
 
 
 def uniform(seed: int, window: int, sequence: int, slot: int) -> float:
@@ -278,14 +279,15 @@ class Verifier:
         return tok, st
 
     def draft_sample(self, draft: torch.Tensor, p: VerifyParams, vocab: int | None = None,
-                     stream=None) -> torch.Tensor:
+                     stream=None, temperature: float = 1.0) -> torch.Tensor:
+        """dsdv_draft_sample(_temperature): tokens[b][j] ~ softmax(draft row / T)."""
         B, G, stride = draft.shape
         vocab = stride if vocab is None else vocab
         cp = p.to_c(B, vocab, stride, _CODE_OF[draft.dtype])
         tokens = torch.empty((B, G), dtype=torch.int32, device=draft.device)
         s = (stream or torch.cuda.current_stream(draft.device)).cuda_stream
-        self._check(LIB.dsdv_draft_sample(self._h, C.byref(cp), draft.data_ptr(),
-                                          tokens.data_ptr(), s))
+        self._check(LIB.dsdv_draft_sample_temperature(self._h, C.byref(cp), float(temperature),
+                                                      draft.data_ptr(), tokens.data_ptr(), s))
         return tokens
 
     def synth_logits(self, batch: int, gamma: int, vocab: int, dtype: torch.dtype,

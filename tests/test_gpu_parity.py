@@ -131,3 +131,25 @@ def test_draft_sample_matches_oracle(verifier, oracle):
     ref = oracle_draft_tokens(oracle, host_rows(draft, V), 21, 3)
     mism = (tok.cpu().numpy() != ref).sum()
     assert mism <= 1, mism
+
+
+@pytest.mark.parametrize("T", [0.0, 0.5, 1.7])
+def test_draft_sample_under_temperature(verifier, ref_oracle, T):
+    """temperature_scale (distribution.cpp:65-97) + inverse CDF on the device,
+    against the reference's own temperature_scale and sample_with_uniform."""
+    from oracle.oracle_lib import window_uniforms
+    from paper_2511_11733_b200.dsdv import VerifyParams
+    from tests.parity_util import host_rows
+    B, G, V = 8, 4, 5000
+    draft, _ = verifier.synth_logits(B, G, V, torch.float32, logits_seed=17)
+    p = VerifyParams(gamma=G, seed=5, window=2)
+    tok = verifier.draft_sample(draft, p, vocab=V, temperature=T).cpu().numpy()
+    rows = host_rows(draft, V)
+    U = window_uniforms(5, 2, B, G)
+    mism = 0
+    for b in range(B):
+        for j in range(G):
+            _, pr = ref_oracle.softmax(rows[b, j])
+            q = ref_oracle.temperature_scale(pr, T)
+            mism += int(ref_oracle.sample_with_uniform(q, U[b, j])[1] != tok[b, j])
+    assert mism <= 1, mism
