@@ -56,19 +56,29 @@ __global__ void __launch_bounds__(17 * 32, 1)
           break;
         }
         if (copy) {
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[st])), "r"(SB) : "memory");
+          // (expect_tx posted after the addresses are known)
           const int half = SB / 2;
           // two rows far apart, like a (draft, target) row pair
           const uint8_t *a, *b;
-          if (rowwise) {  // rows of 256 KB: draft row in the first half, target row in the second
+          uint32_t nbytes = half;
+          if (rowwise == 2) {
+            // the verifier's C2 layout: rows of 128256 bf16 (256512 B), target
+            // [256][9] rows, draft [256][8] rows, position-major items
+            const size_t it2 = item % 2304, jj = it2 / 256, bb = it2 % 256;
+            const size_t RB = 256512, off = (c % 16) * (size_t)half;
+            a = src + (bb * 8 + (jj < 8 ? jj : 0)) * RB + off;
+            b = src + 2048 * RB + (bb * 9 + jj) * RB + off;
+            if (off + half > RB) nbytes = (uint32_t)(RB - off);
+          } else if (rowwise) {  // rows of 256 KB: draft row in the first half, target row in the second
             a = src + (item * 262144 + (c % 16) * half) % (total / 2);
             b = src + total / 2 + (item * 262144 + (c % 16) * half) % (total / 2);
           } else {
             a = src + (c * half) % (total / 2);
             b = src + total / 2 + (c * half) % (total / 2);
           }
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(sm + (size_t)st * SB)), "l"(a), "r"(half), "r"(sa(&full[st])) : "memory");
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(sm + (size_t)st * SB + half)), "l"(b), "r"(half), "r"(sa(&full[st])) : "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[st])), "r"(2 * nbytes) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(sm + (size_t)st * SB)), "l"(a), "r"(nbytes), "r"(sa(&full[st])) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(sm + (size_t)st * SB + half)), "l"(b), "r"(nbytes), "r"(sa(&full[st])) : "memory");
         } else {
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&full[st])) : "memory");
         }
@@ -113,13 +123,14 @@ __global__ void __launch_bounds__(17 * 32, 1)
 int main() {
   const size_t total = (size_t)1 << 30;
   uint8_t *src; unsigned *ticket; float *sink;
-  cudaMalloc(&src, total); cudaMemset(src, 1, total);
+  const size_t alloc = (size_t)(2048 + 2304) * 256512 + (1 << 20);  // the C2 rows
+  cudaMalloc(&src, alloc); cudaMemset(src, 1, alloc);
   cudaMalloc(&ticket, 4); cudaMalloc(&sink, 4);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const int works[] = {48};
-  for (int vary : {0, 1})
-  for (int rowwise : {1})
-  for (int stages : {3, 5, 8}) {
+  const int works[] = {0, 32, 48};
+  for (int vary : {0})
+  for (int rowwise : {1, 2})
+  for (int stages : {5}) {
     const size_t smem = (size_t)32768 * stages + 1024;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int w : works) {
