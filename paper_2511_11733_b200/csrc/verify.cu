@@ -51,7 +51,10 @@ namespace fz {
 #endif
 constexpr int kCW = DSDV_KCW;        // compute warps
 constexpr int kCT = kCW * 32;        // compute threads
-constexpr int kEW = 2;               // epilogue warps (alternate stream items)
+#ifndef DSDV_KEW
+#define DSDV_KEW 2
+#endif
+constexpr int kEW = DSDV_KEW;        // epilogue warps (alternate stream items)
 constexpr int kEpiWarp = kCW;        // first epilogue warp index
 constexpr int kProdWarp = kCW + kEW; // producer warp index
 constexpr int kThreads = (kCW + kEW + 1) * 32;
