@@ -601,7 +601,17 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     }
     const bool last = c == p.n_chunks - 1;
     TR_START(tf);
+#ifdef DSDV_NOFOLD
+    // development probe: a fixed per-chunk busy time instead of the fold
+    {
+      const long long t0 = clock64();
+      while (clock64() - t0 < DSDV_NOFOLD) {
+      }
+    }
+    if (false) {
+#else
     if (kind == kRegular) {
+#endif
       const bool tail = last && (p.vocab_local % CH) != 0;
       Slot<Acc> &sl = sm.slot[s];
       const SlotView sv(sl.area, p.n_chunks * kCW);
@@ -618,8 +628,10 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
                                            sv.bmax[1], trl);
       }
     } else {
+#ifndef DSDV_NOFOLD
       sample_chunk<In>(sm.ring[stage][0], sm.ring[stage][1], c, sm.req[md.req()].wf,
                        reinterpret_cast<double *>(sm.slot[s].area), p, tid, warp, lane);
+#endif
     }
     TR_ADD(trl, kind == kRegular ? kTrComputeFold : kTrComputeSample, tf);
 #ifdef DSDV_TIMELINE
