@@ -370,6 +370,11 @@ __device__ __forceinline__ void capture_row(Slot<Acc> &sl, int r, int lkey, int 
   }
 }
 
+#ifndef DSDV_ZMUFU
+#define DSDV_ZMUFU 3
+#endif
+constexpr int kZMufu = DSDV_ZMUFU;
+
 template <bool PAIR, bool NEEDZ, int VEC>
 __device__ __forceinline__ void exp_sums(const float (&vt)[VEC], const float (&vd)[VEC],
                                          ItemState<float> &S, const DevParams &p) {
@@ -384,7 +389,14 @@ __device__ __forceinline__ void exp_sums(const float (&vt)[VEC], const float (&v
     if (PAIR) {
       const f32x2 xd = fma2(pk2(vd[e], vd[e + 1]), L2, nmd2);
       ad = add2(ad, pk2(fast_exp2(lo2(xd)), fast_exp2(hi2(xd))));
-      if (NEEDZ) az = add2(az, poly_exp2x2(fma2(omt2, xt, mul2(tau2, xd))));
+      if (NEEDZ) {
+        const f32x2 xz = fma2(omt2, xt, mul2(tau2, xd));
+        // kZMufu of the VEC/2 pairs take the MUFU pipe, the rest the FMA pipe
+        if (e / 2 < kZMufu)
+          az = add2(az, pk2(fast_exp2(lo2(xz)), fast_exp2(hi2(xz))));
+        else
+          az = add2(az, poly_exp2x2(xz));
+      }
     }
   }
   S.st += lo2(at) + hi2(at);
