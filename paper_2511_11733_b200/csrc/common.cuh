@@ -70,7 +70,7 @@ struct DevScratch {
   unsigned int *done;        // [B] items finished this window (reset by the finaliser)
   unsigned long long *trace; // [grid][kTraceWords] cycle counters (DSDV_TRACE builds only)
 };
-constexpr int kTraceWords = 24;
+constexpr int kTraceWords = 28;
 
 // ------------------------------------------------------------------ traits
 template <class In>

@@ -73,7 +73,11 @@ constexpr int kSlots = 4;
 // ring depth: 4 x 32 KB stages (3 for fp64 rows, whose slots are larger)
 template <class Acc>
 struct Ring {
+#ifdef DSDV_STAGES  // development probe: ring depth
+  static constexpr int kStages = DSDV_STAGES;
+#else
   static constexpr int kStages = sizeof(Acc) == 8 ? 4 : 5;
+#endif
 };
 constexpr int kMaxTiles = 1024;      // blocks per slot: (chunk, warp), kVecs*32*VEC ids each
 constexpr int kAreaBytes = 8 * kMaxTiles;  // per-slot block maxima (2 x int), or sample tiles (double)
@@ -90,7 +94,8 @@ enum TraceWord : int {
   kTrComputeWaitFull = 0, kTrComputeFold, kTrComputeSample, kTrComputeWaitSlot, kTrComputeItemEnd,
   kTrEpiWaitFull, kTrEpiMerge, kTrEpiTopm, kTrEpiDecide, kTrEpiSample, kTrProdWaitEmpty,
   kTrProdDrain, kTrProdItems, kTrProdSamples, kTrKernel, kTrEpiItems, kTrTopmCand, kTrTopmIns,
-  kTrTopmFallback, kTrMaxSurv, kTrNeedExact, kTrCapCalls, kTrCapLock, kTrCapCycles
+  kTrTopmFallback, kTrMaxSurv, kTrNeedExact, kTrCapCalls, kTrCapLock, kTrCapCycles,
+  kTrComputeLoop, kTrComputeA, kTrComputeB
 };
 #ifdef DSDV_TRACE
 #define TR_START(v) const long long v = clock64()
@@ -498,9 +503,15 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
       bmax_d[c * kCW + warp] = bd;
     }
     const int th0 = vload(&sl.ktheta[0]), th1 = vload(&sl.ktheta[1]);
+#ifdef DSDV_XNOCAP
+    if (false) {  // development probe: capture off (results are wrong)
+#else
     if (bt >= th0 || bd >= th1) {
+#endif
+      TR_START(tcap);
       if (bt >= th0) capture_row<In, TAIL>(sl, 0, lt, th0, vt, starget, c, tid, lane, p, trl);
       if (bd >= th1) capture_row<In, TAIL>(sl, 1, ld, th1, vd, sdraft, c, tid, lane, p, trl);
+      TR_ADD(trl, kTrCapCycles, tcap);
     }
   }
   // lazy online max: one warp vote per chunk, rarely taken
@@ -535,6 +546,10 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
   double ls = 0.0;
+#ifdef DSDV_XNOSAMPLE
+  if (lane == 0) tiles[chunk * kCW + warp] = 1.0;  // development probe (wrong results)
+  return;
+#endif
 #pragma unroll
   for (int h = 0; h < kVecs; ++h) {
     const int q = vec_index(h, warp, lane);
@@ -573,10 +588,16 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
   bool pair = false;
   int kind = kRegular, n = 0, s = 0;
   unsigned long long *trl = (tid & 31) == 0 ? tr : nullptr;
+  TR_START(tloop);
+#ifdef DSDV_TRACE
+  long long tb = clock64();
+#endif
   for (;;) {
+    TR_ADD(trl, kTrComputeB, tb);
     TR_START(tw);
     mbar_wait(&sm.full[stage], phase);
     TR_ADD(trl, kTrComputeWaitFull, tw);
+    TR_START(ta);
 #ifdef DSDV_TIMELINE
     if (trl && warp == 0 && blockIdx.x == 0) {
       unsigned long long *tl = tr + 512 * kTraceWords;
@@ -597,6 +618,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.part_full[ns]);
       }
+      TR_ADD(trl, kTrComputeLoop, tloop);
       break;
     }
     const int c = md.chunk;
@@ -612,6 +634,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       TR_ADD(trl, kTrComputeWaitSlot, ts);
     }
     const bool last = c == p.n_chunks - 1;
+    TR_ADD(trl, kTrComputeA, ta);
     TR_START(tf);
 #ifdef DSDV_NOFOLD
     // development probe: a fixed per-chunk busy time instead of the fold
@@ -659,6 +682,9 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       stage = 0;
       phase ^= 1;
     }
+#ifdef DSDV_TRACE
+    tb = clock64();
+#endif
     if (!last) continue;
 
     // ---- item end: publish this warp's partial, never wait for the epilogue ----
@@ -786,6 +812,9 @@ __device__ __noinline__ void select_topm(Slot<typename InTraits<In>::Acc> &sl, i
     selv[lane] = -INFINITY;
   }
   __syncwarp();
+#ifdef DSDV_XNOCAP
+  return;  // development probe: capture off (results are wrong)
+#endif
   // the final bins hold every block's lane maxima: the tightest bound
   const int th = max(vload(&sl.ktheta[r]), theta_from_bins(sl.klist[r], M, lane));
   const int ncap = vload(&sl.ncap[r]);

@@ -1,5 +1,5 @@
-// Does heavy ALU/MUFU work in 16 consumer warps slow the TMA stream that
-// feeds them? (development aid). Producer: 1 warp, 1-D bulk copies of two
+// foldstream: the overlap probe with the verifier's real fold_chunk as the
+// consumer work (capture pinned off). Does streaming slow the fold? (development aid). Producer: 1 warp, 1-D bulk copies of two
 // 16 KB halves per stage into an S-stage ring, a global ticket over a 1 GB
 // buffer. Consumers: per stage, `work` iterations of an FFMA2 + MUFU mix
 // shaped like the verifier's fold. Reports GB/s with copies, and the time of
@@ -7,8 +7,19 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "../../paper_2511_11733_b200/csrc/verify.cu"
+using namespace dsdv;
+using namespace dsdv::fz;
+__constant__ DevParams cp;
 
 __device__ __forceinline__ uint32_t sa(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void wait_hint(uint64_t *b, uint32_t ph) {
+  uint32_t d = 0;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0,1,0,p; }"
+                 : "=r"(d) : "r"(sa(b)), "r"(ph), "r"(0x989680u) : "memory");
+  } while (!d);
+}
 __device__ __forceinline__ void wait(uint64_t *b, uint32_t ph) {
   uint32_t d = 0;
   do {
@@ -36,6 +47,7 @@ __global__ void __launch_bounds__(17 * 32, 1)
   __syncthreads();
   const size_t nchunks = total / SB;
   if (warp == 16) {
+    if (NOSYNC) return;
     if (lane == 0) {
       int st = 0; uint32_t ph = 0;
       size_t item = 0;
@@ -49,7 +61,11 @@ __global__ void __launch_bounds__(17 * 32, 1)
         } else {
           c = atomicAdd(ticket, 1u);
         }
+#if PRODHINT
+        wait_hint(&empty[st], ph ^ 1);
+#else
         wait(&empty[st], ph ^ 1);
+#endif
         chunk_of[st] = c < nchunks ? (long long)c : -1;
         if (c >= nchunks) {
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&full[st])) : "memory");
@@ -89,10 +105,31 @@ __global__ void __launch_bounds__(17 * 32, 1)
   }
   int st = 0; uint32_t ph = 0;
   float acc = 0.f;
+  __shared__ Slot<float> slot0;
+  __shared__ int bmt[1024], bmd[1024];
+  Slot<float> *sl = &slot0;
+  if (lane < 2) slot0.ktheta[lane] = INT_MAX;
+  ItemState<float> S;
+  S.reset();
   unsigned long long p = 0x3f8000003f800000ull;
   const unsigned long long m = 0x3f7fbe773f7fbe77ull, cc = 0x3a83126f3a83126full;
+#if NOSYNC
+  for (int it = 0; it < 221; ++it) {
+    st = it % stages;
+    fold_chunk<__nv_bfloat16, true, true, false>(sm + (size_t)st * SB, sm + (size_t)st * SB + SB / 2,
+                                                threadIdx.x, 8 + (it & 7), S, cp, warp, lane,
+                                                *sl, bmt, bmd, nullptr);
+    __syncwarp();
+  }
+  if (S.st == 12345.f) sink[0] = S.st + S.sd + S.sz;
+  return;
+#endif
   for (;;) {
+#if CONSHINT
+    wait_hint(&full[st], ph);
+#else
     wait(&full[st], ph);
+#endif
     if (chunk_of[st] < 0) break;
     // read the whole stage like the fold does (4 x LDS.128 per thread)
     float x = 0.f;
@@ -101,40 +138,32 @@ __global__ void __launch_bounds__(17 * 32, 1)
       const uint4 v = *(const uint4 *)(sm + (size_t)st * SB + (q * 512 + threadIdx.x) * 16);
       x += __uint_as_float(v.x ^ v.y ^ v.z ^ v.w) * 1e-30f;
     }
-    // per-warp, per-chunk variable work (like capture calls): work * (0.5 .. 1.5)
-    const unsigned hsh = (unsigned)(chunk_of[st] * 2654435761ull) ^ (warp * 40503u);
-    const int wk = vary ? work / 2 + (int)((hsh >> 7) % (unsigned)(work + 1)) : work;
-    if (work < 0) {  // clock-based busy time (like the verifier's DSDV_NOFOLD probe)
-      const long long t0 = clock64();
-      while (clock64() - t0 < -work) {
-      }
-    }
-    for (int i = 0; i < wk; ++i) {
-      float y;
-      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p) : "l"(m), "l"(cc));
-      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p) : "l"(m), "l"(cc));
-      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p) : "l"(m), "l"(cc));
-      acc += y;
-      x = y * 1e-3f;
+    if (work) {
+      fold_chunk<__nv_bfloat16, true, true, false>(sm + (size_t)st * SB, sm + (size_t)st * SB + SB / 2,
+                                                  threadIdx.x, 8 + (int)(chunk_of[st] & 7), S, cp, warp, lane,
+                                                  *sl, bmt, bmd, nullptr);
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[st])) : "memory");
     if (++st == stages) { st = 0; ph ^= 1; }
   }
-  if (acc == 12345.f) sink[0] = acc + (float)p;
+  if (S.st == 12345.f) sink[0] = S.st + S.sd + S.sz + acc + (float)p;
 }
 
 int main() {
   const size_t total = (size_t)1 << 30;
+  DevParams hp{};
+  hp.B = 1; hp.gamma = 1; hp.V = 128256; hp.vocab_local = 128256; hp.stride = 128256; hp.top_m = 10;
+  hp.n_chunks = 16; hp.tau_f = 0.2f; hp.omt_f = 0.8f;
+  cudaMemcpyToSymbol(cp, &hp, sizeof(hp));
   uint8_t *src; unsigned *ticket; float *sink;
   const size_t alloc = (size_t)(2048 + 2304) * 256512 + (1 << 20);  // the C2 rows
   cudaMalloc(&src, alloc); cudaMemset(src, 1, alloc);
   cudaMalloc(&ticket, 4); cudaMalloc(&sink, 4);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const int works[] = {0, 32, 48, -1500, -2000};
+  const int works[] = {0, 1};
   for (int vary : {0})
-  for (int rowwise : {1, 2})
+  for (int rowwise : {2})
   for (int stages : {5}) {
     const size_t smem = (size_t)32768 * stages + 1024;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -9,7 +9,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2511_11733_b200.dsdv import Verifier, VerifyParams  # noqa: E402
 
 dt = torch.bfloat16 if (sys.argv[1] if len(sys.argv) > 1 else "bf16") == "bf16" else torch.float32
-B, G, V = 256, 8, 128256
+import os
+B, G, V = (int(os.environ.get(k, d)) for k, d in (("B", 256), ("G", 8), ("V", 128256)))
 v = Verifier(0)
 draft, target = v.synth_logits(B, G, V, dt, logits_seed=42)
 p = VerifyParams(gamma=G, tau=0.2, seed=1)

@@ -25,13 +25,13 @@ for w in range(3):
     p.window = w
     v.verify(draft, target, tokens, p, vocab=V, out=out)
 torch.cuda.synchronize()
-buf = np.zeros((1024, 24), dtype=np.uint64)
+buf = np.zeros((1024, 28), dtype=np.uint64)
 lib.dsdv_debug_trace(v._h, buf.ctypes.data, 1024)  # clear
 p.window = 77
 v.verify(draft, target, tokens, p, vocab=V, out=out)
 torch.cuda.synchronize()
 lib.dsdv_debug_trace(v._h, buf.ctypes.data, 1024)
-tl = buf.reshape(-1)[512 * 24: 512 * 24 + 4096].astype(np.int64)
+tl = buf.reshape(-1)[512 * 28: 512 * 28 + 4096].astype(np.int64)
 n = int(min(tl[4094], tl[4095], 1000))
 t = tl[:n * 4].reshape(n, 4)
 issue, ready, waited, done = t[:, 0], t[:, 1], t[:, 2], t[:, 3]

@@ -20,7 +20,7 @@ names = ["compute_wait_full", "compute_fold", "compute_sample", "compute_wait_sl
          "compute_item_end", "epi_wait_full", "epi_merge", "epi_topm", "epi_decide", "epi_sample",
          "prod_wait_empty", "prod_drain", "prod_items", "prod_samples", "kernel", "epi_items",
          "topm_candidates", "topm_survivors", "topm_fallbacks", "max_survivors", "need_exact",
-         "cap_calls", "cap_sorts", "compute_cap"]
+         "cap_calls", "cap_sorts", "compute_cap", "compute_loop", "compute_a", "compute_b"]
 B = int(os.environ.get("B", 256))
 V = int(os.environ.get("V", 128256))
 G = int(os.environ.get("G", 8))
@@ -41,7 +41,7 @@ for w in range(3):
     p.window = w
     v.verify(draft, target, tokens, p, vocab=V, out=out)
 torch.cuda.synchronize()
-buf = np.zeros((1024, 24), dtype=np.uint64)
+buf = np.zeros((1024, 28), dtype=np.uint64)
 lib.dsdv_debug_trace(v._h, buf.ctypes.data, 1024)  # clear
 reps = 5
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
