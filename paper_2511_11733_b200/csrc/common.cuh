@@ -79,16 +79,19 @@ template <>
 struct InTraits<__nv_bfloat16> {
   static constexpr int kVec = 8;  // elements per 16-byte vector
   using Acc = float;
+  __device__ static uint4 neg_inf_vec() { return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u); }
 };
 template <>
 struct InTraits<float> {
   static constexpr int kVec = 4;
   using Acc = float;
+  __device__ static uint4 neg_inf_vec() { return make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u); }
 };
 template <>
 struct InTraits<double> {
   static constexpr int kVec = 2;
   using Acc = double;
+  __device__ static uint4 neg_inf_vec() { return make_uint4(0u, 0xfff00000u, 0u, 0xfff00000u); }
 };
 
 // Unpack one 16-byte vector into accumulator-precision values.
@@ -259,6 +262,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// Expect bytes on the barrier without arriving (the arrival follows later).
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(bytes)
                : "memory");
 }

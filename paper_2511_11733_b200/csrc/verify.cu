@@ -66,6 +66,20 @@ constexpr int kRowBytes = kCT * 16 * kVecs;  // per row per ring stage (16 KB)
 // 16-byte vector h (< kVecs) of (warp, lane) inside a row chunk: each warp owns
 // kVecs * 32 consecutive vectors, so a (chunk, warp) block is a contiguous id
 // range (block maxima, sample tiles), and each LDS.128 is conflict-free.
+// Regular rows whose last chunk is short, ends on a whole 16-byte vector and
+// leaves at most kPadMax bytes of the stage row unused: the producer fills the
+// rest with -inf (a single lane: kept small) and the compute warps fold the
+// chunk without per-element masks. One-chunk rows keep the masked path (their
+// top-m capture starts unbounded, and padding must never enter it).
+constexpr int kPadMax = 4096;
+template <class In>
+__device__ __forceinline__ bool pad_tail(const DevParams &p) {
+  constexpr int CH = kRowBytes / (int)sizeof(In);
+  const int rem = p.vocab_local % CH;
+  return p.n_chunks > 1 && p.vocab_local % InTraits<In>::kVec == 0 && rem != 0 &&
+         (CH - rem) * (int)sizeof(In) <= kPadMax;
+}
+
 __device__ __forceinline__ int vec_index(int h, int warp, int lane) {
   return (warp * kVecs + h) * 32 + lane;
 }
@@ -647,7 +661,9 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
 #else
     if (kind == kRegular) {
 #endif
-      const bool tail = last && (p.vocab_local % CH) != 0;
+      // a short last chunk is masked element by element unless the producer
+      // padded it with -inf (pad_tail)
+      const bool tail = last && (p.vocab_local % CH) != 0 && !pad_tail<In>(p);
       Slot<Acc> &sl = sm.slot[s];
       const SlotView sv(sl.area, p.n_chunks * kCW);
       const uint8_t *sd = sm.ring[stage][0], *st = sm.ring[stage][1];
@@ -657,6 +673,9 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
                                              sv.bmax[1], trl);
         else
           fold_chunk<In, true, NEEDZ, true>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
+                                            sv.bmax[1], trl);
+      } else if (!tail) {
+        fold_chunk<In, false, false, false>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
                                             sv.bmax[1], trl);
       } else {
         fold_chunk<In, false, false, true>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
@@ -1530,7 +1549,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
 template <class In, class Acc = typename InTraits<In>::Acc>
 __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
                                             const In *rd, bool two, int item, int kind, int n,
-                                            int req, int n_chunks, int nlocal, int &stage,
+                                            int req, int n_chunks, int nlocal, bool pad, int &stage,
                                             uint32_t &phase, unsigned long long *tr) {
   constexpr int CH = kRowBytes / (int)sizeof(In);
   for (int c = 0; c < n_chunks; ++c) {
@@ -1553,9 +1572,25 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
       if (q < 1000) tl[q * 4 + 0] = clock64();
     }
 #endif
-    mbar_arrive_expect_tx(&sm.full[stage], two ? 2u * bytes : bytes);
-    bulk_g2s(sm.ring[stage][1], rt + (size_t)c * CH, bytes, &sm.full[stage]);
-    if (two) bulk_g2s(sm.ring[stage][0], rd + (size_t)c * CH, bytes, &sm.full[stage]);
+    if (pad && bytes < (uint32_t)kRowBytes) {
+      // short last chunk of a regular row: the rest of the stage reads as
+      // -inf (no mass, never a maximum), so the compute warps fold it with
+      // the unmasked code; the arrival (release) follows the fill while the
+      // copies run
+      mbar_expect_tx(&sm.full[stage], two ? 2u * bytes : bytes);
+      bulk_g2s(sm.ring[stage][1], rt + (size_t)c * CH, bytes, &sm.full[stage]);
+      if (two) bulk_g2s(sm.ring[stage][0], rd + (size_t)c * CH, bytes, &sm.full[stage]);
+      const uint4 ninf = InTraits<In>::neg_inf_vec();
+      for (uint32_t o = bytes; o < (uint32_t)kRowBytes; o += 16) {
+        *reinterpret_cast<uint4 *>(sm.ring[stage][1] + o) = ninf;
+        if (two) *reinterpret_cast<uint4 *>(sm.ring[stage][0] + o) = ninf;
+      }
+      mbar_arrive(&sm.full[stage]);
+    } else {
+      mbar_arrive_expect_tx(&sm.full[stage], two ? 2u * bytes : bytes);
+      bulk_g2s(sm.ring[stage][1], rt + (size_t)c * CH, bytes, &sm.full[stage]);
+      if (two) bulk_g2s(sm.ring[stage][0], rd + (size_t)c * CH, bytes, &sm.full[stage]);
+    }
     if (++stage == Smem<Acc>::kStages) {
       stage = 0;
       phase ^= 1;
@@ -1585,8 +1620,8 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       const int j = item / p.B, b = item - j * p.B;
       const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
       const In *rd = draft + ((size_t)b * p.gamma + (j < p.gamma ? j : 0)) * (size_t)p.stride;
-      stream_rows<In>(sm, rt, rd, two, item, kSample, n, r, p.n_chunks, p.vocab_local, stage, phase,
-                      tr);
+      stream_rows<In>(sm, rt, rd, two, item, kSample, n, r, p.n_chunks, p.vocab_local, false, stage,
+                      phase, tr);
       TR_INC(tr, kTrProdSamples);
       ++n;
       vstore(&sm.req_head, head + 1);
@@ -1603,8 +1638,8 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
         const bool pair = j < p.gamma;
         const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
         const In *rd = draft + ((size_t)b * p.gamma + (pair ? j : 0)) * (size_t)p.stride;
-        stream_rows<In>(sm, rt, rd, pair, item, kRegular, n, 0, p.n_chunks, p.vocab_local, stage,
-                        phase, tr);
+        stream_rows<In>(sm, rt, rd, pair, item, kRegular, n, 0, p.n_chunks, p.vocab_local,
+                        pad_tail<In>(p), stage, phase, tr);
         TR_INC(tr, kTrProdItems);
         ++n;
         continue;
