@@ -29,6 +29,7 @@
 namespace dsdv {
 
 constexpr int kMaxShards = 64;
+constexpr int kStageCand = 64;  // staged slice candidates per row (P * top_m)
 
 struct MergeIn {
   const double *rec;   // rank 0's [B][G1][kRecordWords] partial records
@@ -60,6 +61,9 @@ __global__ void __launch_bounds__(1024)
   using Acc = typename InTraits<In>::Acc;
   __shared__ PosSummary summ[32];
   __shared__ int tset[32][kMaxTopM];
+  // one row's P slice lists staged per warp (P * M <= kStageCand)
+  __shared__ double cand_v[32][kStageCand];
+  __shared__ int cand_i[32][kStageCand];
   __shared__ SampleShared samp;
   __shared__ Weigher<Acc> wf;
   __shared__ int s_pos;
@@ -123,12 +127,31 @@ __global__ void __launch_bounds__(1024)
     if (pair) {
       const int nc = in.P * M;
       const size_t lo = ((size_t)b * G + j) * 2 * M;
+      const bool staged = nc <= kStageCand;
       for (int r = 0; r < 2; ++r) {  // 0: target, 1: draft
+        if (staged) {
+          // the P sorted lists of this row into shared memory (one coalesced
+          // pass), so the ranking below reads no global memory
+          for (int c = lane; c < nc; c += 32) {
+            const int q = c / M, i = c - q * M;
+            const int id = in.topi[q * in.topi_stride + lo + r * M + i];
+            cand_i[warp][c] = id;
+            cand_v[warp][c] = id >= 0 ? in.topv[q * in.topv_stride + lo + r * M + i] : 0.0;
+          }
+          __syncwarp();
+        }
         for (int c = lane; c < ((nc + 31) & ~31); c += 32) {
           const bool val = c < nc;
           const int q = val ? c / M : 0, i = val ? c - (c / M) * M : 0;
-          const int id = val ? in.topi[q * in.topi_stride + lo + r * M + i] : -1;
-          const double v = val && id >= 0 ? in.topv[q * in.topv_stride + lo + r * M + i] : 0.0;
+          int id;
+          double v;
+          if (staged) {
+            id = val ? cand_i[warp][c] : -1;
+            v = val && id >= 0 ? cand_v[warp][c] : 0.0;
+          } else {
+            id = val ? in.topi[q * in.topi_stride + lo + r * M + i] : -1;
+            v = val && id >= 0 ? in.topv[q * in.topv_stride + lo + r * M + i] : 0.0;
+          }
           int rank = 0;
           if (id >= 0) {
             for (int qq = 0; qq < in.P; ++qq) {
@@ -136,12 +159,18 @@ __global__ void __launch_bounds__(1024)
                 rank += i;  // own list is sorted: its first i entries beat it
                 continue;
               }
-              const int32_t *ti = in.topi + qq * in.topi_stride + lo + r * M;
-              const double *tv = in.topv + qq * in.topv_stride + lo + r * M;
               for (int ii = 0; ii < M; ++ii) {
-                const int id2 = ti[ii];
-                if (id2 < 0) break;
-                const double v2 = tv[ii];
+                int id2;
+                double v2;
+                if (staged) {
+                  id2 = cand_i[warp][qq * M + ii];
+                  if (id2 < 0) break;
+                  v2 = cand_v[warp][qq * M + ii];
+                } else {
+                  id2 = in.topi[qq * in.topi_stride + lo + r * M + ii];
+                  if (id2 < 0) break;
+                  v2 = in.topv[qq * in.topv_stride + lo + r * M + ii];
+                }
                 if (!(v2 > v || (v2 == v && id2 < id))) break;  // sorted: no later entry beats it
                 ++rank;
               }
@@ -158,6 +187,7 @@ __global__ void __launch_bounds__(1024)
             shared += __popc(__ballot_sync(0xffffffffu, hit));
           }
         }
+        __syncwarp();  // the staged lists are overwritten by the next row
         if (r == 0) {
           // fewer than M valid candidates: the rest of the set stays unmatched
           __syncwarp();

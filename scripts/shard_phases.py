@@ -48,6 +48,7 @@ for it in range(13):
     if it >= 3:
         for i in range(len(names)):
             acc[i] += ev[i].elapsed_time(ev[i + 1]) / 10
+print(f"rank {comm.rank} stats {acc[0]:.3f} ms", flush=True)
 if comm.rank == 0:
     print("P=%d B=%d: " % (comm.size, B) + ", ".join(f"{k} {t:.3f} ms" for k, t in zip(names, acc)),
           f"total {sum(acc):.3f} ms")
