@@ -331,7 +331,8 @@ def run_sharded(args, rank, world, local_rank):
 
     def step(w):
         p.window = w
-        return sv.verify(draft, target, tokens, p, V, lo, n, comm, stream=stream)
+        return sv.verify(draft, target, tokens, p, V, lo, n, comm, stream=stream,
+                         exchange=args.exchange)
 
     for w in range(args.warmup):
         out = step(10_000 + w)
@@ -354,6 +355,8 @@ def run_sharded(args, rank, world, local_rank):
     mean_k = float(out.accepted_count.float().mean().item())
     committed = float((out.accepted_count.float() + 1).sum().item())
     bad = int((out.status != 0).sum().item())
+    if args.exchange == "peer":
+        bad += int(sv._peer_status.item() != 0)  # a peer flag never arrived
 
     # e2e: this rank's slice and the tokens from pinned host memory, results back
     draft_h, target_h, tokens_h = (draft.cpu().pin_memory(), target.cpu().pin_memory(),
@@ -370,7 +373,8 @@ def run_sharded(args, rank, world, local_rank):
         d_target.copy_(target_h, non_blocking=True)
         d_tokens.copy_(tokens_h, non_blocking=True)
         p.window = w
-        o = sv.verify(d_draft, d_target, d_tokens, p, V, lo, n, comm, stream=stream)
+        o = sv.verify(d_draft, d_target, d_tokens, p, V, lo, n, comm, stream=stream,
+                      exchange=args.exchange)
         for k, h in res_h.items():
             h.copy_(getattr(o, k), non_blocking=True)
 
@@ -403,8 +407,13 @@ def run_sharded(args, rank, world, local_rank):
                                f"({n} ids on rank 0), B={Bt} (256 per GPU), gamma=8, bf16 logits, "
                                "tau=0.2, lambda=(2.0, 0.2, 0.5), top_m=10",
                    "batch_total": Bt, "gamma": GAMMA, "vocab": V, "vocab_per_rank": n,
-                   "parallelism": f"vocab-sharded tp{world} (NCCL: 4 all-gathers + 1 all-reduce "
-                                  "per window)",
+                   "parallelism": (f"vocab-sharded tp{world} (records: fused NVLink peer "
+                                   "stores from the stats kernel + flags; NCCL: 1 all-gather "
+                                   "of [B] masses + 1 all-reduce per window)")
+                   if args.exchange == "peer" else
+                   (f"vocab-sharded tp{world} (NCCL: 2 all-gathers + 1 all-reduce "
+                    "per window)"),
+                   "exchange": args.exchange,
                    "l2": "no flush needed: 1.12 GB of logits per GPU per step > 126 MB L2",
                    "mean_accepted_k": mean_k, "status_errors": bad,
                    "committed_tokens_per_s": committed / (ms_max * 1e-3)},
@@ -478,6 +487,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--parallel", choices=["vocab", "replicas"], default="vocab",
                     help="N>1: vocabulary-sharded window (C4) or independent replicas")
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                    help="vocab: partial records by the stats kernel's own NVLink stores into "
+                         "every rank's buffer (CUDA IPC), or by an NCCL all-gather")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)

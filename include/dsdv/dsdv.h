@@ -226,6 +226,38 @@ dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t n
                              int32_t *position, double *uniform, double *mass_out,
                              double *tile_scratch, void *stream);
 enum { DSDV_SHARD_MASS = 0, DSDV_SHARD_RESOLVE = 1 };
+
+/* ---- peer exchange over NVLink (one process per GPU) ---------------------
+ * Replaces the record all-gather: every rank maps every rank's exchange
+ * buffer (CUDA IPC) and the stats kernel stores its partial records straight
+ * into all of them, item by item, while it streams (fused compute + exchange).
+ * Exchange buffer of rank q: [nranks][rank_stride_bytes] packed records (the
+ * dsdv_shard_stats layout at off_records / off_top_values / off_top_ids inside
+ * each rank's slot), then nranks uint64 arrival flags at nranks * stride. */
+#define DSDV_MAX_PEERS 8
+dsdv_status dsdv_dev_alloc(dsdv_ctx *ctx, uint64_t bytes, void **dev_ptr); /* zeroed */
+dsdv_status dsdv_dev_free(dsdv_ctx *ctx, void *dev_ptr);
+dsdv_status dsdv_ipc_handle(dsdv_ctx *ctx, void *dev_ptr, uint8_t handle[64]);
+dsdv_status dsdv_ipc_open(dsdv_ctx *ctx, const uint8_t handle[64], void **dev_ptr);
+dsdv_status dsdv_ipc_close(dsdv_ctx *ctx, void *dev_ptr);
+/* rank_bases[q]: rank q's exchange buffer as mapped in this process (q ==
+ * rank: the local one). The records of this rank land in slot `rank` of all. */
+dsdv_status dsdv_shard_stats_peers(dsdv_ctx *ctx, const dsdv_params *params,
+                                   const void *draft_logits, const void *target_logits,
+                                   const int32_t *draft_tokens, int32_t nranks, int32_t rank,
+                                   void *const *rank_bases, uint64_t rank_stride_bytes,
+                                   uint64_t off_records, uint64_t off_top_values,
+                                   uint64_t off_top_ids, void *stream);
+/* After the stats pass on `stream`: flag `rank` in every rank's buffer = epoch
+ * (system-scope release). */
+dsdv_status dsdv_peer_signal(dsdv_ctx *ctx, int32_t nranks, int32_t rank,
+                             void *const *rank_bases, uint64_t rank_stride_bytes, uint64_t epoch,
+                             void *stream);
+/* Holds `stream` until every flag of the local buffer reached epoch (acquire);
+ * after timeout_ns, *status (device) = DSDV_E_NCCL and the stream continues. */
+dsdv_status dsdv_peer_wait(dsdv_ctx *ctx, int32_t nranks, void *local_base,
+                           uint64_t rank_stride_bytes, uint64_t epoch, uint64_t timeout_ns,
+                           int32_t *status, void *stream);
 /* MASS: mass_out[b] = this slice's weight total of row position[b].
  * RESOLVE: masses_all = the gathered [nranks][B] totals; token_out[b] = the
  * global id on the owning rank, -1 elsewhere; status[b] = DSDV_E_EMPTY_RESIDUAL

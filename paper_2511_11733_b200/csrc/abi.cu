@@ -38,6 +38,10 @@ cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nran
 cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, double tau,
                             double *out, int32_t *status, cudaStream_t stream);
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t stream);
+cudaError_t launch_peer_signal(char *const *bases, int nranks, int rank, unsigned long long stride,
+                               unsigned long long epoch, cudaStream_t stream);
+cudaError_t launch_peer_wait(const unsigned long long *flags, int nranks, unsigned long long epoch,
+                             unsigned long long timeout_ns, int *status, cudaStream_t stream);
 cudaError_t launch_synth(int dtype, int B, int gamma, int V, int stride, uint64_t seed,
                          void *draft, void *target, cudaStream_t stream);
 }  // namespace dsdv
@@ -182,7 +186,8 @@ bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draft,
                       const void *target, const int32_t *tokens, const dsdv_outputs *out,
                       void *stream, bool stats_only, double *topv = nullptr,
-                      int32_t *topi = nullptr) {
+                      int32_t *topi = nullptr, int npeer = 0,
+                      const long long *peer_delta = nullptr) {
   const bool partial = topv != nullptr;
   if (!ctx) return DSDV_E_INVARIANT;
   DevParams d;
@@ -230,6 +235,8 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   DevOut o = to_dev(out);
   o.topv = topv;
   o.topi = topi;
+  o.npeer = npeer;
+  for (int q = 0; q < npeer; ++q) o.peer_delta[q] = peer_delta[q];
   switch (params->dtype) {
     case DSDV_DTYPE_BF16:
       e = dsdv::launch_fused<__nv_bfloat16>(d, draft, target, tokens, o, s, (cudaStream_t)stream,
@@ -418,6 +425,105 @@ dsdv_status dsdv_shard_stats(dsdv_ctx *ctx, const dsdv_params *params, const voi
   out.records = records;
   return run_fused(ctx, params, draft_logits, target_logits, draft_tokens, &out, stream, true,
                    top_values, top_ids);
+}
+
+dsdv_status dsdv_dev_alloc(dsdv_ctx *ctx, uint64_t bytes, void **dev_ptr) {
+  if (!ctx || !dev_ptr || !bytes) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = cudaMalloc(dev_ptr, bytes);
+  if (e == cudaSuccess) e = cudaMemset(*dev_ptr, 0, bytes);
+  return e == cudaSuccess ? DSDV_OK : cuda_fail(ctx, e, "dsdv_dev_alloc");
+}
+
+dsdv_status dsdv_dev_free(dsdv_ctx *ctx, void *dev_ptr) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = cudaFree(dev_ptr);
+  return e == cudaSuccess ? DSDV_OK : cuda_fail(ctx, e, "dsdv_dev_free");
+}
+
+dsdv_status dsdv_ipc_handle(dsdv_ctx *ctx, void *dev_ptr, uint8_t handle[64]) {
+  if (!ctx || !dev_ptr || !handle) return DSDV_E_INVARIANT;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaIpcGetMemHandle");
+  std::memcpy(handle, &h, 64);
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_ipc_open(dsdv_ctx *ctx, const uint8_t handle[64], void **dev_ptr) {
+  if (!ctx || !dev_ptr || !handle) return DSDV_E_INVARIANT;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? DSDV_OK : cuda_fail(ctx, e, "cudaIpcOpenMemHandle");
+}
+
+dsdv_status dsdv_ipc_close(dsdv_ctx *ctx, void *dev_ptr) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = cudaIpcCloseMemHandle(dev_ptr);
+  return e == cudaSuccess ? DSDV_OK : cuda_fail(ctx, e, "cudaIpcCloseMemHandle");
+}
+
+dsdv_status dsdv_shard_stats_peers(dsdv_ctx *ctx, const dsdv_params *params,
+                                   const void *draft_logits, const void *target_logits,
+                                   const int32_t *draft_tokens, int32_t nranks, int32_t rank,
+                                   void *const *rank_bases, uint64_t rank_stride_bytes,
+                                   uint64_t off_records, uint64_t off_top_values,
+                                   uint64_t off_top_ids, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  if (nranks < 1 || nranks > DSDV_MAX_PEERS || rank < 0 || rank >= nranks || !rank_bases)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_stats_peers: bad rank set (nranks <= %d)",
+                DSDV_MAX_PEERS);
+  if (off_records % 8 || off_top_values % 8 || off_top_ids % 4 || rank_stride_bytes % 8)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_stats_peers: misaligned layout");
+  for (int q = 0; q < nranks; ++q)
+    if (!rank_bases[q]) return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_stats_peers: null base");
+  char *own = (char *)rank_bases[rank] + (size_t)rank * rank_stride_bytes;
+  long long delta[DSDV_MAX_PEERS];
+  int np = 0;
+  for (int q = 0; q < nranks; ++q)
+    if (q != rank)
+      delta[np++] = (long long)(((char *)rank_bases[q] + (size_t)rank * rank_stride_bytes) - own);
+  dsdv_outputs out;
+  std::memset(&out, 0, sizeof(out));
+  out.records = (double *)(own + off_records);
+  return run_fused(ctx, params, draft_logits, target_logits, draft_tokens, &out, stream, true,
+                   (double *)(own + off_top_values), (int32_t *)(own + off_top_ids), np, delta);
+}
+
+dsdv_status dsdv_peer_signal(dsdv_ctx *ctx, int32_t nranks, int32_t rank,
+                             void *const *rank_bases, uint64_t rank_stride_bytes, uint64_t epoch,
+                             void *stream) {
+  if (!ctx || nranks < 1 || nranks > DSDV_MAX_PEERS || rank < 0 || rank >= nranks || !rank_bases)
+    return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess)
+    e = dsdv::launch_peer_signal((char *const *)rank_bases, nranks, rank,
+                                 (unsigned long long)rank_stride_bytes, (unsigned long long)epoch,
+                                 (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "peer signal launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_peer_wait(dsdv_ctx *ctx, int32_t nranks, void *local_base,
+                           uint64_t rank_stride_bytes, uint64_t epoch, uint64_t timeout_ns,
+                           int32_t *status, void *stream) {
+  if (!ctx || nranks < 1 || nranks > DSDV_MAX_PEERS || !local_base) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess)
+    e = dsdv::launch_peer_wait(
+        (const unsigned long long *)((char *)local_base + (size_t)nranks * rank_stride_bytes),
+        nranks, (unsigned long long)epoch, (unsigned long long)timeout_ns, status,
+        (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "peer wait launch");
+  ctx->launches += 1;
+  return DSDV_OK;
 }
 
 dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,

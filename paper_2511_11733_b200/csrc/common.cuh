@@ -60,6 +60,10 @@ struct DevOut {
       *p_effective_y, *uniform, *records;
   double *topv;    // sharded partial: [B][gamma][2][M] top-m values (target, draft)
   int32_t *topi;   //                  and global ids
+  // peer exchange: every partial store is repeated at address + peer_delta[q]
+  // (the same slot in rank q's mapped exchange buffer), q < npeer
+  int npeer;
+  long long peer_delta[8];
 };
 
 struct DevScratch {

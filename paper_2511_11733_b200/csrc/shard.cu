@@ -491,4 +491,59 @@ template cudaError_t launch_shard_sample<double>(const DevParams &, int, int, in
                                                  int32_t *, int32_t *, const double *,
                                                  cudaStream_t);
 
+// ------------------------------------------------------------------ peer exchange
+struct PeerBases {
+  char *base[8];
+};
+
+// Flag `rank` of every rank's exchange buffer = epoch (after the stats pass
+// on this stream: its peer stores were fenced at system scope per item).
+__global__ void peer_signal_kernel(PeerBases pb, int nranks, int rank, unsigned long long stride,
+                                   unsigned long long epoch) {
+  const int q = threadIdx.x;
+  if (q >= nranks) return;
+  __threadfence_system();
+  unsigned long long *f =
+      reinterpret_cast<unsigned long long *>(pb.base[q] + (size_t)nranks * stride) + rank;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+}
+
+// Hold the stream until every rank's flag reached epoch, at most timeout_ns.
+__global__ void peer_wait_kernel(const unsigned long long *flags, int nranks,
+                                 unsigned long long epoch, unsigned long long timeout_ns,
+                                 int *status) {
+  const int q = threadIdx.x;
+  if (q < nranks) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+      if (v >= epoch) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        if (status) atomicExch(status, DSDV_E_NCCL);
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+cudaError_t launch_peer_signal(char *const *bases, int nranks, int rank, unsigned long long stride,
+                               unsigned long long epoch, cudaStream_t stream) {
+  PeerBases pb{};
+  for (int q = 0; q < nranks; ++q) pb.base[q] = bases[q];
+  peer_signal_kernel<<<1, 32, 0, stream>>>(pb, nranks, rank, stride, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const unsigned long long *flags, int nranks, unsigned long long epoch,
+                             unsigned long long timeout_ns, int *status, cudaStream_t stream) {
+  peer_wait_kernel<<<1, 32, 0, stream>>>(flags, nranks, epoch, timeout_ns, status);
+  return cudaGetLastError();
+}
+
 }  // namespace dsdv

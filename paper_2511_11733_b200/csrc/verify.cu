@@ -1309,35 +1309,47 @@ __device__ __noinline__ void write_partial(const DevOut &o, const DevParams &p, 
     }
   }
   const int G1 = p.gamma + 1;
+  // one store here and one per peer (fused exchange: the records reach every
+  // rank's buffer while the pass streams)
+  auto put = [&](auto *addr, auto v) {
+    *addr = v;
+    for (int q = 0; q < o.npeer; ++q)
+      *reinterpret_cast<decltype(addr)>(reinterpret_cast<char *>(addr) + o.peer_delta[q]) = v;
+  };
   if (lane == 0) {
     double *r = o.records + ((size_t)b * G1 + j) * kRecordWords;
-    r[0] = Mt;
-    r[1] = (MtL + log2(St)) * kLn2 - dd * Mt - Mt;
+    double w[kRecordWords];
+    w[0] = Mt;
+    w[1] = (MtL + log2(St)) * kLn2 - dd * Mt - Mt;
     if (pair) {
       const int y = tokens[(size_t)b * p.gamma + j];
       const int yl = y - p.vocab_offset;
       const bool own = yl >= 0 && yl < p.vocab_local;
-      r[2] = Md;
-      r[3] = (MdL + log2(Sd)) * kLn2 - dd * Md - Md;
-      r[4] = lsz;
-      r[5] = own ? load_scalar<In>(rt + yl) : NAN;
-      r[6] = own ? load_scalar<In>(rd + yl) : NAN;
-      r[7] = (double)((diff ? 1 : 0) | (own ? 2 : 0));
+      w[2] = Md;
+      w[3] = (MdL + log2(Sd)) * kLn2 - dd * Md - Md;
+      w[4] = lsz;
+      w[5] = own ? load_scalar<In>(rt + yl) : NAN;
+      w[6] = own ? load_scalar<In>(rd + yl) : NAN;
+      w[7] = (double)((diff ? 1 : 0) | (own ? 2 : 0));
     } else {
-      r[2] = r[3] = r[4] = 0.0;
-      r[5] = r[6] = NAN;
-      r[7] = 0.0;
+      w[2] = w[3] = w[4] = 0.0;
+      w[5] = w[6] = NAN;
+      w[7] = 0.0;
     }
+#pragma unroll
+    for (int k = 0; k < kRecordWords; ++k) put(r + k, w[k]);
   }
   const int M = p.top_m;
   if (pair && lane < M) {
     const size_t base = ((size_t)b * p.gamma + j) * 2 * M;
     const int it = es.sel[0][lane], id = es.sel[1][lane];
-    o.topv[base + lane] = es.selv[0][lane];
-    o.topi[base + lane] = it >= 0 ? p.vocab_offset + it : -1;
-    o.topv[base + M + lane] = es.selv[1][lane];
-    o.topi[base + M + lane] = id >= 0 ? p.vocab_offset + id : -1;
+    put(o.topv + base + lane, es.selv[0][lane]);
+    put(o.topi + base + lane, it >= 0 ? p.vocab_offset + it : -1);
+    put(o.topv + base + M + lane, es.selv[1][lane]);
+    put(o.topi + base + M + lane, id >= 0 ? p.vocab_offset + id : -1);
   }
+  // (no fence per item: dsdv_peer_signal, after this kernel on the stream,
+  // fences at system scope and releases the arrival flags)
 }
 
 template <class In>
@@ -1543,6 +1555,9 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       atomicAdd(&sm.epi_count, 1);
     }
   }
+  // peer exchange: this warp's stores into the other ranks' buffers are
+  // visible system-wide before the kernel ends (dsdv_peer_signal follows)
+  if (o.npeer) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ producer warp

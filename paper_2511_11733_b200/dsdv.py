@@ -90,6 +90,15 @@ def _load() -> C.CDLL:
         "dsdv_mix_rows": (st, [vp, C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp, vp]),
         "dsdv_spin": (st, [vp, C.c_uint64, vp]),
         "dsdv_draft_sample_temperature": (st, [vp, C.POINTER(_Params), C.c_double, vp, vp, vp]),
+        "dsdv_dev_alloc": (st, [vp, C.c_uint64, C.POINTER(vp)]),
+        "dsdv_dev_free": (st, [vp, vp]),
+        "dsdv_ipc_handle": (st, [vp, vp, vp]),
+        "dsdv_ipc_open": (st, [vp, vp, C.POINTER(vp)]),
+        "dsdv_ipc_close": (st, [vp, vp]),
+        "dsdv_shard_stats_peers": (st, [vp, C.POINTER(_Params), vp, vp, vp, C.c_int32, C.c_int32,
+                                        vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp]),
+        "dsdv_peer_signal": (st, [vp, C.c_int32, C.c_int32, vp, C.c_uint64, C.c_uint64, vp]),
+        "dsdv_peer_wait": (st, [vp, C.c_int32, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -103,7 +112,9 @@ EXPORTED = ("dsdv_create", "dsdv_destroy", "dsdv_last_error", "dsdv_abi_version"
             "dsdv_verify", "dsdv_window_stats", "dsdv_sample_extra", "dsdv_draft_sample",
             "dsdv_sync", "dsdv_uniform", "dsdv_synth_logits", "dsdv_launch_count",
             "dsdv_shard_stats", "dsdv_shard_merge", "dsdv_shard_sample", "dsdv_mix_rows",
-            "dsdv_spin", "dsdv_draft_sample_temperature")
+            "dsdv_spin", "dsdv_draft_sample_temperature", "dsdv_dev_alloc", "dsdv_dev_free",
+            "dsdv_ipc_handle", "dsdv_ipc_open", "dsdv_ipc_close", "dsdv_shard_stats_peers",
+            "dsdv_peer_signal", "dsdv_peer_wait")
 
 
 def uniform(seed: int, window: int, sequence: int, slot: int) -> float:

@@ -62,6 +62,73 @@ class TorchComm:
         return t
 
 
+class PeerExchange:
+    """Exchange buffers of all ranks mapped into this process (CUDA IPC over
+    NVLink): the stats kernel of every rank stores its packed records straight
+    into slot `rank` of each rank's buffer (dsdv_shard_stats_peers), then a
+    flag per rank (dsdv_peer_signal / dsdv_peer_wait) replaces the record
+    all-gather. Two buffer sets alternate by window (the next window's stores
+    never touch the set a slower peer may still be merging).
+
+    `bases` may also be given directly: P virtual ranks in one process on one
+    device (tests), where no IPC mapping is needed."""
+
+    def __init__(self, verifier: Verifier, nranks: int, rank: int, size: int,
+                 comm: "TorchComm | None" = None, bases: list[int] | None = None):
+        self.v, self.P, self.rank = verifier, nranks, rank
+        self.stride = -(-size // 256) * 256
+        self.set_bytes = self.P * self.stride
+        self.bytes = 2 * self.set_bytes + 8 * self.P  # two sets, then the flags
+        self._owned, self._opened = [], []
+        if bases is not None:
+            self.bases = list(bases)
+            return
+        ptr = C.c_void_p()
+        self.v._check(LIB.dsdv_dev_alloc(self.v._h, self.bytes, C.byref(ptr)))
+        self._owned.append(ptr.value)
+        handle = (C.c_uint8 * 64)()
+        self.v._check(LIB.dsdv_ipc_handle(self.v._h, ptr, handle))
+        mine = torch.tensor(bytearray(handle), dtype=torch.uint8, device=verifier.device)
+        allh = comm.all_gather(mine).cpu()
+        self.bases = []
+        for q in range(self.P):
+            if q == rank:
+                self.bases.append(ptr.value)
+                continue
+            h = (C.c_uint8 * 64)(*allh[q].tolist())
+            peer = C.c_void_p()
+            self.v._check(LIB.dsdv_ipc_open(self.v._h, h, C.byref(peer)))
+            self._opened.append(peer.value)
+            self.bases.append(peer.value)
+
+    @staticmethod
+    def allocate_local(verifier: Verifier, nranks: int, size: int) -> list[int]:
+        """P exchange buffers on this device (the single-process emulation)."""
+        stride = -(-size // 256) * 256
+        out = []
+        for _ in range(nranks):
+            ptr = C.c_void_p()
+            verifier._check(LIB.dsdv_dev_alloc(verifier._h, 2 * nranks * stride + 8 * nranks,
+                                               C.byref(ptr)))
+            out.append(ptr.value)
+        return out
+
+    def set_bases(self, epoch: int) -> list[int]:
+        off = (epoch & 1) * self.set_bytes
+        return [b + off for b in self.bases]
+
+    def flag_bases(self) -> list[int]:
+        """Bases whose [P * stride] offset is the flag array (signal / wait)."""
+        return [b + 2 * self.set_bytes - self.P * self.stride for b in self.bases]
+
+    def close(self):
+        for ptr in self._opened:
+            LIB.dsdv_ipc_close(self.v._h, C.c_void_p(ptr))
+        for ptr in self._owned:
+            LIB.dsdv_dev_free(self.v._h, C.c_void_p(ptr))
+        self._opened, self._owned = [], []
+
+
 class ShardedVerifier:
     """One rank of the vocabulary-sharded verifier."""
 
@@ -98,9 +165,35 @@ class ShardedVerifier:
                                            base + o_tv, base + o_ti, s))
         return buf
 
+    def stats_peers(self, ex: PeerExchange, epoch: int, draft, target, tokens,
+                    p: VerifyParams, vocab: int, offset: int, local: int, stream=None):
+        """dsdv_shard_stats_peers: this rank's records into every rank's buffer
+        set `epoch & 1`, then its arrival flag (epoch) in every rank's buffer."""
+        B, G, _ = draft.shape
+        M = min(p.top_m, vocab)
+        cp = self._cp(p, draft, target, tokens, vocab, offset, local)
+        (o_rec, o_tv, o_ti), size = self.packed_layout(B, G, M)
+        assert ex.stride >= size
+        s = (stream or torch.cuda.current_stream(draft.device)).cuda_stream
+        bases = (C.c_void_p * ex.P)(*ex.set_bases(epoch))
+        self.v._check(LIB.dsdv_shard_stats_peers(
+            self.v._h, C.byref(cp), draft.data_ptr(), target.data_ptr(), tokens.data_ptr(), ex.P,
+            ex.rank, bases, ex.stride, o_rec, o_tv, o_ti, s))
+        flags = (C.c_void_p * ex.P)(*ex.flag_bases())
+        self.v._check(LIB.dsdv_peer_signal(self.v._h, ex.P, ex.rank, flags, ex.stride, epoch, s))
+
+    def wait_peers(self, ex: PeerExchange, epoch: int, status: torch.Tensor, stream=None,
+                   timeout_s: float = 10.0):
+        """Hold the stream until every rank's records of `epoch` have landed."""
+        s = (stream or torch.cuda.current_stream(status.device)).cuda_stream
+        local = ex.flag_bases()[ex.rank]
+        self.v._check(LIB.dsdv_peer_wait(self.v._h, ex.P, C.c_void_p(local), ex.stride, epoch,
+                                         int(timeout_s * 1e9), status.data_ptr(), s))
+
     def merge(self, draft, target, tokens, p: VerifyParams, vocab: int, offset: int, local: int,
-              packed_all: torch.Tensor, out: WindowResult | None = None, stream=None):
-        """dsdv_shard_merge over the gathered packed buffers [P][size]."""
+              packed_all: torch.Tensor | tuple, out: WindowResult | None = None, stream=None):
+        """dsdv_shard_merge over the gathered packed buffers [P][size], or over
+        (base pointer, P, stride) of a peer-exchange buffer set."""
         B, G, _ = draft.shape
         M = min(p.top_m, vocab)
         cp = self._cp(p, draft, target, tokens, vocab, offset, local)
@@ -112,11 +205,14 @@ class ShardedVerifier:
         # tile sums of each extra-draw row, reused by the owner's RESOLVE
         self._tiles = torch.empty((B, TILE_WORDS), dtype=torch.float64, device=draft.device)
         (o_rec, o_tv, o_ti), size = self.packed_layout(B, G, M)
-        assert packed_all.is_contiguous() and packed_all.shape[-1] == size
-        base = packed_all.data_ptr()
+        if isinstance(packed_all, tuple):
+            base, nranks, stride = packed_all
+        else:
+            assert packed_all.is_contiguous() and packed_all.shape[-1] == size
+            base, nranks, stride = packed_all.data_ptr(), packed_all.shape[0], size
         s = (stream or torch.cuda.current_stream(draft.device)).cuda_stream
-        self.v._check(LIB.dsdv_shard_merge(self.v._h, C.byref(cp), packed_all.shape[0],
-                                           base + o_rec, base + o_tv, base + o_ti, size,
+        self.v._check(LIB.dsdv_shard_merge(self.v._h, C.byref(cp), nranks,
+                                           base + o_rec, base + o_tv, base + o_ti, stride,
                                            draft.data_ptr(), target.data_ptr(), tokens.data_ptr(),
                                            C.byref(out._c), position.data_ptr(), u.data_ptr(),
                                            mass.data_ptr(), self._tiles.data_ptr(), s))
@@ -140,10 +236,28 @@ class ShardedVerifier:
 
     # ---- one window on this rank --------------------------------------------
     def verify(self, draft, target, tokens, p: VerifyParams, vocab: int, offset: int, local: int,
-               comm: TorchComm, out: WindowResult | None = None, stream=None) -> WindowResult:
-        packed = self.stats(draft, target, tokens, p, vocab, offset, local, stream)
+               comm: TorchComm, out: WindowResult | None = None, stream=None,
+               exchange: str = "nccl") -> WindowResult:
+        """One window on this rank. exchange="peer": the records travel by the
+        stats kernel's own NVLink stores (PeerExchange) instead of an all-gather."""
+        if exchange == "peer":
+            B, G, _ = draft.shape
+            _, size = self.packed_layout(B, G, min(p.top_m, vocab))
+            ex = getattr(self, "_ex", None)
+            if ex is None or ex.stride < size:
+                ex = self._ex = PeerExchange(self.v, comm.size, comm.rank, size, comm=comm)
+                self._epoch = 0
+                self._peer_status = torch.zeros(1, dtype=torch.int32, device=draft.device)
+            self._epoch += 1
+            self.stats_peers(ex, self._epoch, draft, target, tokens, p, vocab, offset, local,
+                             stream)
+            self.wait_peers(ex, self._epoch, self._peer_status, stream)
+            merged_in = (ex.set_bases(self._epoch)[ex.rank], ex.P, ex.stride)
+        else:
+            packed = self.stats(draft, target, tokens, p, vocab, offset, local, stream)
+            merged_in = comm.all_gather(packed)
         out, position, u, mass = self.merge(draft, target, tokens, p, vocab, offset, local,
-                                            comm.all_gather(packed), out, stream)
+                                            merged_in, out, stream)
         masses = comm.all_gather(mass)
         tok = self.sample(SHARD_RESOLVE, comm.rank, comm.size, draft, target, tokens, p, vocab,
                           offset, local, out, position, u, masses, stream=stream,
@@ -159,6 +273,42 @@ def contiguous_slice(rows: torch.Tensor, lo: int, n: int) -> torch.Tensor:
     out = torch.full((*rows.shape[:-1], stride), float("-inf"), dtype=rows.dtype,
                      device=rows.device)
     out[..., :n] = rows[..., lo:lo + n]
+    return out
+
+
+def shard_slices_peer(verifier: Verifier, draft: torch.Tensor, target: torch.Tensor,
+                      tokens: torch.Tensor, p: VerifyParams, vocab: int, nranks: int,
+                      epoch: int = 1) -> WindowResult:
+    """shard_slices with the peer exchange: every virtual rank's stats pass
+    stores its records into all P exchange buffers (plain device buffers of this
+    process instead of IPC mappings), flags arrive, each rank merges its own."""
+    B, G, _ = draft.shape
+    _, size = ShardedVerifier.packed_layout(B, G, min(p.top_m, vocab))
+    bases = PeerExchange.allocate_local(verifier, nranks, size)
+    exs = [PeerExchange(verifier, nranks, r, size, bases=bases) for r in range(nranks)]
+    svs = [ShardedVerifier(verifier) for _ in range(nranks)]
+    parts = []
+    for r in range(nranks):
+        lo, n = slice_bounds(vocab, nranks, r)
+        parts.append((lo, n, contiguous_slice(draft, lo, n), contiguous_slice(target, lo, n)))
+    for r, (lo, n, d, t) in enumerate(parts):
+        svs[r].stats_peers(exs[r], epoch, d, t, tokens, p, vocab, lo, n)
+    status = torch.zeros(1, dtype=torch.int32, device=draft.device)
+    merged = []
+    for r, (lo, n, d, t) in enumerate(parts):
+        svs[r].wait_peers(exs[r], epoch, status, timeout_s=2.0)
+        merged.append(svs[r].merge(d, t, tokens, p, vocab, lo, n,
+                                   (exs[r].set_bases(epoch)[r], nranks, exs[r].stride)))
+    masses = torch.stack([m[3] for m in merged])
+    toks = torch.stack([svs[r].sample(SHARD_RESOLVE, r, nranks, d, t, tokens, p, vocab, lo, n,
+                                      *merged[r][:3], masses, tiles=svs[r]._tiles)
+                        for r, (lo, n, d, t) in enumerate(parts)])
+    out = merged[0][0]
+    out.extra_token.copy_(toks.max(dim=0).values)
+    torch.cuda.synchronize(draft.device)
+    assert int(status.item()) == 0, "peer wait timed out"
+    for b in bases:
+        LIB.dsdv_dev_free(verifier._h, C.c_void_p(b))
     return out
 
 

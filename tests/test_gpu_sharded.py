@@ -47,3 +47,25 @@ def test_sharded_equals_unsharded_gpu(verifier, oracle):
     same = float((gpu["accepted_count"] == uns["accepted_count"]).float().mean())
     assert same >= 0.95
     assert bool((gpu["norm_match"] == uns["norm_match"]).all())
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_peer_exchange_equals_gathered(verifier, oracle, P):
+    """The fused exchange (stats kernel storing into every rank's buffer,
+    flags, merge from the local buffer) gives the gathered path's window bit
+    for bit, and stays parity-green against the oracle."""
+    from paper_2511_11733_b200.sharded import shard_slices_peer
+    crit = Oracle.crit(2.0, 0.2, 0.5, 10)
+    d64, t64, toks, unsharded, (draft, target, tokens, p) = run_gpu_window(
+        verifier, torch.bfloat16, 16, 4, 32000, 0.2, crit, seed=3, oracle=oracle)
+    ref = shard_slices(verifier, draft, target, tokens, p, 32000, P).to_host()
+    for epoch in (1, 2, 3):  # both buffer sets, advancing flags
+        got = shard_slices_peer(verifier, draft, target, tokens, p, 32000, P, epoch=epoch)
+        got = got.to_host()
+        assert set(got) == set(ref)
+        for k in ref:
+            a, b = torch.as_tensor(got[k]), torch.as_tensor(ref[k])
+            assert torch.equal(a, b) or (a.is_floating_point() and
+                                         torch.equal(a.nan_to_num(7.0), b.nan_to_num(7.0))), k
+    rep = compare_window(oracle, d64, t64, toks, got, 0.2, crit, 3, 0)
+    assert rep.ok(), rep.mismatches[:5]
