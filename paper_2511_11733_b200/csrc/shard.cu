@@ -29,7 +29,8 @@
 namespace dsdv {
 
 constexpr int kMaxShards = 64;
-constexpr int kStageCand = 64;  // staged slice candidates per row (P * top_m)
+constexpr int kStageCand = 128;  // staged slice candidates per row (P * top_m)
+constexpr int kStageWarps = 16;  // positions staged (gamma + 1 <= 16)
 
 struct MergeIn {
   const double *rec;   // rank 0's [B][G1][kRecordWords] partial records
@@ -62,8 +63,8 @@ __global__ void __launch_bounds__(1024)
   __shared__ PosSummary summ[32];
   __shared__ int tset[32][kMaxTopM];
   // one row's P slice lists staged per warp (P * M <= kStageCand)
-  __shared__ double cand_v[32][kStageCand];
-  __shared__ int cand_i[32][kStageCand];
+  __shared__ double cand_v[kStageWarps][kStageCand];
+  __shared__ int cand_i[kStageWarps][kStageCand];
   __shared__ SampleShared samp;
   __shared__ Weigher<Acc> wf;
   __shared__ int s_pos;
@@ -127,7 +128,54 @@ __global__ void __launch_bounds__(1024)
     if (pair) {
       const int nc = in.P * M;
       const size_t lo = ((size_t)b * G + j) * 2 * M;
-      const bool staged = nc <= kStageCand;
+      const bool staged = nc <= kStageCand && warp < kStageWarps;
+      if (staged && in.P <= 32) {
+        // P-way merge of the sorted slice lists: lane q holds the head of
+        // list q, M warp arg-max steps (value desc, id asc) give the top M
+        for (int r = 0; r < 2; ++r) {
+          for (int c = lane; c < nc; c += 32) {
+            const int q = c / M, i = c - q * M;
+            const int id = in.topi[q * in.topi_stride + lo + r * M + i];
+            cand_i[warp][c] = id;
+            cand_v[warp][c] = id >= 0 ? in.topv[q * in.topv_stride + lo + r * M + i] : 0.0;
+          }
+          if (r == 0 && lane < M) tset[warp][lane] = -1;
+          __syncwarp();
+          int head = 0;
+          for (int k = 0; k < M; ++k) {
+            double bv = -INFINITY;
+            int bid = -1, bl = 32;
+            if (lane < in.P && head < M) {
+              const int id = cand_i[warp][lane * M + head];
+              if (id >= 0) {
+                bv = cand_v[warp][lane * M + head];
+                bid = id;
+                bl = lane;
+              }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+              const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+              const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+              if (ol < 32 && (bl == 32 || ov > bv || (ov == bv && oid < bid))) {
+                bv = ov;
+                bid = oid;
+                bl = ol;
+              }
+            }
+            if (bl == 32) break;  // every list exhausted (slices shorter than M)
+            if (lane == bl) ++head;
+            if (r == 0) {
+              if (lane == 0) tset[warp][k] = bid;
+            } else {
+              __syncwarp();
+              shared += __ballot_sync(0xffffffffu, lane < M && tset[warp][lane] == bid) ? 1 : 0;
+            }
+          }
+          __syncwarp();
+        }
+      } else
       for (int r = 0; r < 2; ++r) {  // 0: target, 1: draft
         if (staged) {
           // the P sorted lists of this row into shared memory (one coalesced
