@@ -143,25 +143,50 @@ __global__ void __launch_bounds__(1024)
           __syncwarp();
           int head = 0;
           for (int k = 0; k < M; ++k) {
-            double bv = -INFINITY;
             int bid = -1, bl = 32;
-            if (lane < in.P && head < M) {
-              const int id = cand_i[warp][lane * M + head];
-              if (id >= 0) {
-                bv = cand_v[warp][lane * M + head];
-                bid = id;
-                bl = lane;
+            if (sizeof(Acc) == 4) {
+              // fp32 logits: (value desc, id asc) as one 64-bit key, a
+              // branch-free warp max (0 = empty, below every real key)
+              unsigned long long key = 0ull;
+              if (lane < in.P && head < M) {
+                const int id = cand_i[warp][lane * M + head];
+                if (id >= 0) {
+                  const unsigned fb = __float_as_uint((float)cand_v[warp][lane * M + head]);
+                  const unsigned ord = (fb & 0x80000000u) ? ~fb : (fb | 0x80000000u);
+                  key = ((unsigned long long)ord << 32) | (unsigned)(~id);
+                }
               }
-            }
+              unsigned long long best = key;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-              const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
-              const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-              if (ol < 32 && (bl == 32 || ov > bv || (ov == bv && oid < bid))) {
-                bv = ov;
-                bid = oid;
-                bl = ol;
+              for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+                best = other > best ? other : best;
+              }
+              if (best != 0ull) {
+                bid = (int)~(unsigned)best;
+                const unsigned who = __ballot_sync(0xffffffffu, key == best);
+                bl = __ffs(who) - 1;
+              }
+            } else {
+              double bv = -INFINITY;
+              if (lane < in.P && head < M) {
+                const int id = cand_i[warp][lane * M + head];
+                if (id >= 0) {
+                  bv = cand_v[warp][lane * M + head];
+                  bid = id;
+                  bl = lane;
+                }
+              }
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                if (ol < 32 && (bl == 32 || ov > bv || (ov == bv && oid < bid))) {
+                  bv = ov;
+                  bid = oid;
+                  bl = ol;
+                }
               }
             }
             if (bl == 32) break;  // every list exhausted (slices shorter than M)
