@@ -341,10 +341,12 @@ def run_sharded(args, rank, world, local_rank):
     launches0 = ver.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
+        h0 = time.perf_counter()
         e0.record(stream)
         for k in range(args.steps):
             out = step(k)
         e1.record(stream)
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # enqueue rate
         torch.cuda.synchronize(device)
     dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -416,6 +418,7 @@ def run_sharded(args, rank, world, local_rank):
                    "exchange": args.exchange,
                    "l2": "no flush needed: 1.12 GB of logits per GPU per step > 126 MB L2",
                    "mean_accepted_k": mean_k, "status_errors": bad,
+                   "host_enqueue_ms_per_step": host_ms,
                    "committed_tokens_per_s": committed / (ms_max * 1e-3)},
         "roofline": {"bound": "hbm", "achieved": alg_bytes / (ms_max * 1e-3) / 1e9, "peak": hbm,
                      "unit": "GB/s", "frac": alg_bytes / (ms_max * 1e-3) / 1e9 / hbm,

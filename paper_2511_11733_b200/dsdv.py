@@ -173,22 +173,30 @@ class WindowResult:
     @staticmethod
     def allocate(batch: int, gamma: int, device, per_position: bool = True,
                  records: bool = False) -> "WindowResult":
-        i32 = dict(dtype=torch.int32, device=device)
-        r = WindowResult(
-            accepted_count=torch.zeros(batch, **i32), extra_token=torch.zeros(batch, **i32),
-            extra_source=torch.zeros(batch, dtype=torch.uint8, device=device),
-            key_count=torch.zeros(batch, **i32), status=torch.zeros(batch, **i32),
-            near_threshold=torch.zeros(batch, **i32))
-        if per_position:
-            shp = (batch, gamma)
-            r.key_mask = torch.zeros(shp, dtype=torch.uint8, device=device)
-            r.accepted = torch.zeros(shp, dtype=torch.uint8, device=device)
-            for n in ("accept_prob", "h_target", "h_draft", "p_target_y", "p_draft_y",
-                      "norm_match", "p_effective_y", "uniform"):
-                setattr(r, n, torch.zeros(shp, dtype=torch.float64, device=device))
+        """Zeroed outputs carved from one buffer (one fill launch, not one per field)."""
+        f64 = (["accept_prob", "h_target", "h_draft", "p_target_y", "p_draft_y", "norm_match",
+                "p_effective_y", "uniform"] if per_position else [])
+        plan = [(n, torch.float64, (batch, gamma)) for n in f64]
         if records:
-            r.records = torch.zeros((batch, gamma + 1, RECORD_WORDS), dtype=torch.float64,
-                                    device=device)
+            plan.append(("records", torch.float64, (batch, gamma + 1, RECORD_WORDS)))
+        plan += [(n, torch.int32, (batch,)) for n in
+                 ("accepted_count", "extra_token", "key_count", "status", "near_threshold")]
+        plan.append(("extra_source", torch.uint8, (batch,)))
+        if per_position:
+            plan += [("key_mask", torch.uint8, (batch, gamma)), ("accepted", torch.uint8, (batch, gamma))]
+        sizes = []
+        for _, dt, shp in plan:
+            n = 1
+            for d in shp:
+                n *= d
+            sizes.append(n * torch.empty((), dtype=dt).element_size())
+        buf = torch.zeros(sum(-(-x // 8) * 8 for x in sizes), dtype=torch.uint8, device=device)
+        r = WindowResult(*[None] * 6)
+        off = 0
+        for (name, dt, shp), nbytes in zip(plan, sizes):
+            setattr(r, name, buf[off:off + nbytes].view(dt).view(shp))
+            off += -(-nbytes // 8) * 8
+        r._buf = buf
         r._c = _Outputs(*[(getattr(r, n).data_ptr() if getattr(r, n) is not None else None)
                           for n, _ in _OUT_FIELDS])
         return r
