@@ -1316,9 +1316,8 @@ __device__ __noinline__ void write_partial(const DevOut &o, const DevParams &p, 
     for (int q = 0; q < o.npeer; ++q)
       *reinterpret_cast<decltype(addr)>(reinterpret_cast<char *>(addr) + o.peer_delta[q]) = v;
   };
+  double w[kRecordWords];
   if (lane == 0) {
-    double *r = o.records + ((size_t)b * G1 + j) * kRecordWords;
-    double w[kRecordWords];
     w[0] = Mt;
     w[1] = (MtL + log2(St)) * kLn2 - dd * Mt - Mt;
     if (pair) {
@@ -1336,9 +1335,15 @@ __device__ __noinline__ void write_partial(const DevOut &o, const DevParams &p, 
       w[5] = w[6] = NAN;
       w[7] = 0.0;
     }
-#pragma unroll
-    for (int k = 0; k < kRecordWords; ++k) put(r + k, w[k]);
   }
+  // one coalesced store of the record per destination (lane k: word k)
+  double wk = 0.0;
+#pragma unroll
+  for (int k = 0; k < kRecordWords; ++k) {
+    const double t = __shfl_sync(0xffffffffu, w[k], 0);
+    if (lane == k) wk = t;
+  }
+  if (lane < kRecordWords) put(o.records + ((size_t)b * G1 + j) * kRecordWords + lane, wk);
   const int M = p.top_m;
   if (pair && lane < M) {
     const size_t base = ((size_t)b * p.gamma + j) * 2 * M;
