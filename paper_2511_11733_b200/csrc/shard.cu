@@ -52,8 +52,10 @@ struct PosSummary {
   int err, key, kind, near, accepted;
 };
 
-template <class In>
-__global__ void __launch_bounds__(1024)
+// MAXT: the block size bound the registers are sized for (gamma + 1 <= 10
+// position warps fit 320 threads and four CTAs per SM; larger gamma uses 1024)
+template <class In, int MAXT = 1024, int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB)
     shard_merge_kernel(const __grid_constant__ DevParams p, const MergeIn in,
                        const In *__restrict__ draft, const In *__restrict__ target,
                        const int32_t *__restrict__ tokens, const DevOut o,
@@ -521,7 +523,12 @@ cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const doub
     in.topi_stride = rank_bytes / 4;
   }
   const int threads = 32 * G1 > kConsumerThreads ? 32 * G1 : kConsumerThreads;
-  shard_merge_kernel<In><<<p.B, threads, 0, stream>>>(p, in, (const In *)draft,
+  if (threads <= 320)
+    shard_merge_kernel<In, 320, 4><<<p.B, threads, 0, stream>>>(p, in, (const In *)draft,
+                                                               (const In *)target, tokens, o,
+                                                               position, uniform, mass_out, tiles);
+  else
+    shard_merge_kernel<In><<<p.B, threads, 0, stream>>>(p, in, (const In *)draft,
                                                       (const In *)target, tokens, o, position,
                                                       uniform, mass_out, tiles);
   return cudaGetLastError();
