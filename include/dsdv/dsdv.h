@@ -253,6 +253,32 @@ dsdv_status dsdv_shard_stats_peers(dsdv_ctx *ctx, const dsdv_params *params,
 dsdv_status dsdv_peer_signal(dsdv_ctx *ctx, int32_t nranks, int32_t rank,
                              void *const *rank_bases, uint64_t rank_stride_bytes, uint64_t epoch,
                              void *stream);
+/* The merge and the RESOLVE step over the same buffers: the merge reads the
+ * records from the local buffer (every rank's slot) and stores this slice's
+ * [B] masses at off_mass of slot `rank` in every buffer; RESOLVE reads the
+ * masses from the local buffer and stores its [B] tokens (-1 where this rank
+ * is not the owner) at off_tokens of slot `rank` in every buffer;
+ * dsdv_peer_tokens_max folds the P token arrays of the local buffer. With
+ * dsdv_peer_signal / dsdv_peer_wait between the steps, a window needs no
+ * collective call. */
+dsdv_status dsdv_shard_merge_peers(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
+                                   int32_t rank, void *const *rank_bases,
+                                   uint64_t rank_stride_bytes, uint64_t off_records,
+                                   uint64_t off_top_values, uint64_t off_top_ids,
+                                   uint64_t off_mass, const void *draft_logits,
+                                   const void *target_logits, const int32_t *draft_tokens,
+                                   const dsdv_outputs *out, int32_t *position, double *uniform,
+                                   double *tile_scratch, void *stream);
+dsdv_status dsdv_shard_resolve_peers(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
+                                     int32_t rank, void *const *rank_bases,
+                                     uint64_t rank_stride_bytes, uint64_t off_mass,
+                                     uint64_t off_tokens, const void *draft_logits,
+                                     const void *target_logits, const double *records,
+                                     const int32_t *position, const double *uniform,
+                                     int32_t *status, const double *tile_scratch, void *stream);
+dsdv_status dsdv_peer_tokens_max(dsdv_ctx *ctx, int32_t nranks, void *local_base,
+                                 uint64_t rank_stride_bytes, uint64_t off_tokens, int32_t batch,
+                                 int32_t *token_out, void *stream);
 /* Holds `stream` until every flag of the local buffer reached epoch (acquire);
  * after timeout_ns, *status (device) = DSDV_E_NCCL and the stream continues. */
 dsdv_status dsdv_peer_wait(dsdv_ctx *ctx, int32_t nranks, void *local_base,

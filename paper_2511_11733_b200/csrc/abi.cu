@@ -28,13 +28,18 @@ cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const doub
                                const int32_t *topi, int P, size_t rank_bytes, const void *draft,
                                const void *target, const int32_t *tokens, const DevOut &o,
                                int32_t *position, double *uniform, double *mass_out,
-                               double *tiles, cudaStream_t stream);
+                               double *tiles, cudaStream_t stream,
+                               const long long *mass_delta = nullptr, int n_delta = 0);
 template <class In>
 cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nranks,
                                 const void *draft, const void *target, const double *records,
                                 const int32_t *position, const double *uniform,
                                 const double *masses, double *mass_out, int32_t *token_out,
-                                int32_t *status, const double *tiles, cudaStream_t stream);
+                                int32_t *status, const double *tiles, cudaStream_t stream,
+                                const long long *tok_delta = nullptr, int n_delta = 0,
+                                size_t mstride = 0);
+cudaError_t launch_tokens_max(const int32_t *tok, size_t stride_elems, int nranks, int B,
+                              int32_t *out, cudaStream_t stream);
 cudaError_t launch_mix_rows(int kind, int V, const double *a, const double *b, double tau,
                             double *out, int32_t *status, cudaStream_t stream);
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t stream);
@@ -526,13 +531,14 @@ dsdv_status dsdv_peer_wait(dsdv_ctx *ctx, int32_t nranks, void *local_base,
   return DSDV_OK;
 }
 
-dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
-                             const double *records_all, const double *top_values_all,
-                             const int32_t *top_ids_all, uint64_t rank_stride_bytes,
-                             const void *draft_logits, const void *target_logits,
-                             const int32_t *draft_tokens, const dsdv_outputs *out,
-                             int32_t *position, double *uniform, double *mass_out,
-                             double *tile_scratch, void *stream) {
+static dsdv_status shard_merge_impl(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
+                                    const double *records_all, const double *top_values_all,
+                                    const int32_t *top_ids_all, uint64_t rank_stride_bytes,
+                                    const void *draft_logits, const void *target_logits,
+                                    const int32_t *draft_tokens, const dsdv_outputs *out,
+                                    int32_t *position, double *uniform, double *mass_out,
+                                    double *tile_scratch, void *stream,
+                                    const long long *mass_delta, int n_delta) {
   if (!ctx) return DSDV_E_INVARIANT;
   DevParams d;
   dsdv_status st = build_params(ctx, params, d);
@@ -552,19 +558,21 @@ dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t n
       e = dsdv::launch_shard_merge<__nv_bfloat16>(d, records_all, top_values_all, top_ids_all,
                                                   nranks, (size_t)rank_stride_bytes, draft_logits,
                                                   target_logits, draft_tokens, o, position,
-                                                  uniform, mass_out, tile_scratch, (cudaStream_t)stream);
+                                                  uniform, mass_out, tile_scratch, (cudaStream_t)stream,
+                                                  mass_delta, n_delta);
       break;
     case DSDV_DTYPE_F32:
       e = dsdv::launch_shard_merge<float>(d, records_all, top_values_all, top_ids_all, nranks,
                                           (size_t)rank_stride_bytes, draft_logits, target_logits,
                                           draft_tokens, o, position, uniform, mass_out,
-                                          tile_scratch, (cudaStream_t)stream);
+                                          tile_scratch, (cudaStream_t)stream, mass_delta, n_delta);
       break;
     default:
       e = dsdv::launch_shard_merge<double>(d, records_all, top_values_all, top_ids_all, nranks,
                                            (size_t)rank_stride_bytes, draft_logits, target_logits,
                                            draft_tokens, o, position, uniform, mass_out,
-                                           tile_scratch, (cudaStream_t)stream);
+                                           tile_scratch, (cudaStream_t)stream, mass_delta,
+                                           n_delta);
       break;
   }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "shard_merge launch");
@@ -572,12 +580,26 @@ dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t n
   return DSDV_OK;
 }
 
-dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t mode, int32_t rank,
-                              int32_t nranks, const void *draft_logits, const void *target_logits,
-                              const double *records, const int32_t *position,
-                              const double *uniform, const double *masses_all, double *mass_out,
-                              int32_t *token_out, int32_t *status, const double *tile_scratch,
-                              void *stream) {
+dsdv_status dsdv_shard_merge(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
+                             const double *records_all, const double *top_values_all,
+                             const int32_t *top_ids_all, uint64_t rank_stride_bytes,
+                             const void *draft_logits, const void *target_logits,
+                             const int32_t *draft_tokens, const dsdv_outputs *out,
+                             int32_t *position, double *uniform, double *mass_out,
+                             double *tile_scratch, void *stream) {
+  return shard_merge_impl(ctx, params, nranks, records_all, top_values_all, top_ids_all,
+                          rank_stride_bytes, draft_logits, target_logits, draft_tokens, out,
+                          position, uniform, mass_out, tile_scratch, stream, nullptr, 0);
+}
+
+static dsdv_status shard_sample_impl(dsdv_ctx *ctx, const dsdv_params *params, int32_t mode,
+                                     int32_t rank, int32_t nranks, const void *draft_logits,
+                                     const void *target_logits, const double *records,
+                                     const int32_t *position, const double *uniform,
+                                     const double *masses_all, double *mass_out,
+                                     int32_t *token_out, int32_t *status,
+                                     const double *tile_scratch, void *stream,
+                                     const long long *tok_delta, int n_delta, size_t mstride) {
   if (!ctx) return DSDV_E_INVARIANT;
   DevParams d;
   dsdv_status st = build_params(ctx, params, d);
@@ -597,20 +619,104 @@ dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t 
       e = dsdv::launch_shard_sample<__nv_bfloat16>(d, mode, rank, nranks, draft_logits,
                                                    target_logits, records, position, uniform,
                                                    masses_all, mass_out, token_out, status,
-                                                   tile_scratch, (cudaStream_t)stream);
+                                                   tile_scratch, (cudaStream_t)stream, tok_delta,
+                                                   n_delta, mstride);
       break;
     case DSDV_DTYPE_F32:
       e = dsdv::launch_shard_sample<float>(d, mode, rank, nranks, draft_logits, target_logits,
                                            records, position, uniform, masses_all, mass_out,
-                                           token_out, status, tile_scratch, (cudaStream_t)stream);
+                                           token_out, status, tile_scratch, (cudaStream_t)stream,
+                                           tok_delta, n_delta, mstride);
       break;
     default:
       e = dsdv::launch_shard_sample<double>(d, mode, rank, nranks, draft_logits, target_logits,
                                             records, position, uniform, masses_all, mass_out,
-                                            token_out, status, tile_scratch, (cudaStream_t)stream);
+                                            token_out, status, tile_scratch, (cudaStream_t)stream,
+                                            tok_delta, n_delta, mstride);
       break;
   }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "shard_sample launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_shard_sample(dsdv_ctx *ctx, const dsdv_params *params, int32_t mode, int32_t rank,
+                              int32_t nranks, const void *draft_logits, const void *target_logits,
+                              const double *records, const int32_t *position,
+                              const double *uniform, const double *masses_all, double *mass_out,
+                              int32_t *token_out, int32_t *status, const double *tile_scratch,
+                              void *stream) {
+  return shard_sample_impl(ctx, params, mode, rank, nranks, draft_logits, target_logits, records,
+                           position, uniform, masses_all, mass_out, token_out, status,
+                           tile_scratch, stream, nullptr, 0, 0);
+}
+
+// slot `rank` of every rank's exchange buffer, relative to this rank's own slot
+static int peer_deltas(void *const *rank_bases, int nranks, int rank, uint64_t stride,
+                       long long *delta) {
+  const char *own = (const char *)rank_bases[rank] + (size_t)rank * stride;
+  int np = 0;
+  for (int q = 0; q < nranks; ++q)
+    if (q != rank) delta[np++] = (long long)(((const char *)rank_bases[q] + (size_t)rank * stride) - own);
+  return np;
+}
+
+dsdv_status dsdv_shard_merge_peers(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
+                                   int32_t rank, void *const *rank_bases,
+                                   uint64_t rank_stride_bytes, uint64_t off_records,
+                                   uint64_t off_top_values, uint64_t off_top_ids,
+                                   uint64_t off_mass, const void *draft_logits,
+                                   const void *target_logits, const int32_t *draft_tokens,
+                                   const dsdv_outputs *out, int32_t *position, double *uniform,
+                                   double *tile_scratch, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  if (nranks < 1 || nranks > DSDV_MAX_PEERS || rank < 0 || rank >= nranks || !rank_bases ||
+      off_mass % 8 || rank_stride_bytes % 8)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_merge_peers: bad rank set or layout");
+  const char *local = (const char *)rank_bases[rank];
+  long long delta[DSDV_MAX_PEERS];
+  const int np = peer_deltas(rank_bases, nranks, rank, rank_stride_bytes, delta);
+  double *mass_own = (double *)(local + (size_t)rank * rank_stride_bytes + off_mass);
+  return shard_merge_impl(ctx, params, nranks, (const double *)(local + off_records),
+                          (const double *)(local + off_top_values),
+                          (const int32_t *)(local + off_top_ids), rank_stride_bytes, draft_logits,
+                          target_logits, draft_tokens, out, position, uniform, mass_own,
+                          tile_scratch, stream, delta, np);
+}
+
+dsdv_status dsdv_shard_resolve_peers(dsdv_ctx *ctx, const dsdv_params *params, int32_t nranks,
+                                     int32_t rank, void *const *rank_bases,
+                                     uint64_t rank_stride_bytes, uint64_t off_mass,
+                                     uint64_t off_tokens, const void *draft_logits,
+                                     const void *target_logits, const double *records,
+                                     const int32_t *position, const double *uniform,
+                                     int32_t *status, const double *tile_scratch, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  if (nranks < 1 || nranks > DSDV_MAX_PEERS || rank < 0 || rank >= nranks || !rank_bases ||
+      off_mass % 8 || off_tokens % 4 || rank_stride_bytes % 8)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_resolve_peers: bad rank set or layout");
+  const char *local = (const char *)rank_bases[rank];
+  long long delta[DSDV_MAX_PEERS];
+  const int np = peer_deltas(rank_bases, nranks, rank, rank_stride_bytes, delta);
+  int32_t *tok_own = (int32_t *)(local + (size_t)rank * rank_stride_bytes + off_tokens);
+  return shard_sample_impl(ctx, params, DSDV_SHARD_RESOLVE, rank, nranks, draft_logits,
+                           target_logits, records, position, uniform,
+                           (const double *)(local + off_mass), nullptr, tok_own, status,
+                           tile_scratch, stream, delta, np, (size_t)(rank_stride_bytes / 8));
+}
+
+dsdv_status dsdv_peer_tokens_max(dsdv_ctx *ctx, int32_t nranks, void *local_base,
+                                 uint64_t rank_stride_bytes, uint64_t off_tokens, int32_t batch,
+                                 int32_t *token_out, void *stream) {
+  if (!ctx || nranks < 1 || nranks > DSDV_MAX_PEERS || !local_base || !token_out || batch < 1 ||
+      off_tokens % 4 || rank_stride_bytes % 4)
+    return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess)
+    e = dsdv::launch_tokens_max((const int32_t *)((const char *)local_base + off_tokens),
+                                (size_t)(rank_stride_bytes / 4), nranks, batch, token_out,
+                                (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "tokens max launch");
   ctx->launches += 1;
   return DSDV_OK;
 }

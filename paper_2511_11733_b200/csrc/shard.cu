@@ -52,6 +52,18 @@ struct PosSummary {
   int err, key, kind, near, accepted;
 };
 
+// Peer exchange of the [B]-sized results: every store is repeated at
+// address + d[q] (the same slot of rank q's mapped exchange buffer).
+struct PeerDelta {
+  long long d[8];
+  int n;
+};
+template <class T>
+__device__ __forceinline__ void put_peers(T *a, T v, const PeerDelta &pd) {
+  *a = v;
+  for (int q = 0; q < pd.n; ++q) *reinterpret_cast<T *>(reinterpret_cast<char *>(a) + pd.d[q]) = v;
+}
+
 // MAXT: the block size bound the registers are sized for (gamma + 1 <= 10
 // position warps fit 320 threads and four CTAs per SM; larger gamma uses 1024)
 template <class In, int MAXT = 1024, int MINB = 1>
@@ -60,7 +72,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
                        const In *__restrict__ draft, const In *__restrict__ target,
                        const int32_t *__restrict__ tokens, const DevOut o,
                        int32_t *__restrict__ position, double *__restrict__ uniform,
-                       double *__restrict__ mass_out, double *__restrict__ tiles) {
+                       double *__restrict__ mass_out, double *__restrict__ tiles,
+                       const PeerDelta mpd) {
   using Acc = typename InTraits<In>::Acc;
   __shared__ PosSummary summ[32];
   __shared__ int tset[32][kMaxTopM];
@@ -404,7 +417,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
   // ---- this slice's mass of the extra-draw row (fused MASS step) ----
   const int pos = s_pos;
   if (pos < 0) {
-    if (threadIdx.x == 0) mass_out[b] = 0.0;
+    if (threadIdx.x == 0) {
+      put_peers(mass_out + b, 0.0, mpd);
+      if (mpd.n) __threadfence_system();
+    }
     return;
   }
   if (threadIdx.x >= kConsumerThreads) return;
@@ -413,7 +429,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
   int near = 0;
   cdf_sample<In, Acc>(rt, rd, wf, p.vocab_local, 0.0, p.eps_u, &samp, threadIdx.x, &near, -1.0,
                       tiles ? tiles + (size_t)b * (kMaxTiles + 2) : nullptr);
-  if (threadIdx.x == 0) mass_out[b] = samp.W;
+  if (threadIdx.x == 0) {
+    put_peers(mass_out + b, samp.W, mpd);
+    if (mpd.n) __threadfence_system();
+  }
 }
 
 // Extra draw over a sharded row. MASS: the slice's weight total. RESOLVE: the
@@ -426,7 +445,8 @@ __global__ void __launch_bounds__(kConsumerThreads)
                         const double *__restrict__ records, const int32_t *__restrict__ position,
                         const double *__restrict__ uniform, const double *__restrict__ masses,
                         double *__restrict__ mass_out, int32_t *__restrict__ token_out,
-                        int32_t *__restrict__ status, const double *__restrict__ tiles) {
+                        int32_t *__restrict__ status, const double *__restrict__ tiles,
+                        const PeerDelta tpd, size_t mstride) {
   using Acc = typename InTraits<In>::Acc;
   __shared__ SampleShared samp;
   __shared__ Weigher<Acc> wf;
@@ -441,7 +461,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     if (j < 0 || j > G) {
       skip = 1;
       if (mode == 0) mass_out[b] = 0.0;
-      else token_out[b] = -1;
+      else put_peers(token_out + b, -1, tpd);
     } else {
       const double *r = records + ((size_t)b * G1 + j) * kRecordWords;
       const int kind = (int)r[kRecFlags] & 0xff;
@@ -457,12 +477,12 @@ __global__ void __launch_bounds__(kConsumerThreads)
       if (mode == 1) {
         // owner of T = u W: the first slice whose cumulative mass passes T
         double W = 0.0;
-        for (int q = 0; q < nranks; ++q) W += masses[(size_t)q * p.B + b];
+        for (int q = 0; q < nranks; ++q) W += masses[(size_t)q * mstride + b];
         const double T = uniform[b] * W;
         int owner = -1, last = -1;
         double cum = 0.0, base = 0.0;
         for (int q = 0; q < nranks; ++q) {
-          const double w = masses[(size_t)q * p.B + b];
+          const double w = masses[(size_t)q * mstride + b];
           if (w > 0.0) {
             last = q;
             if (owner < 0 && cum + w > T) {
@@ -474,16 +494,16 @@ __global__ void __launch_bounds__(kConsumerThreads)
         }
         if (!(W > 0.0)) {
           skip = 1;
-          token_out[b] = -1;
+          put_peers(token_out + b, -1, tpd);
           status[b] = DSDV_E_EMPTY_RESIDUAL;
         } else {
           if (owner < 0) {  // rounding gap above the total: the last supported slice
             owner = last;
-            base = cum - masses[(size_t)last * p.B + b];
+            base = cum - masses[(size_t)last * mstride + b];
           }
           if (owner != rank) {
             skip = 1;
-            token_out[b] = -1;
+            put_peers(token_out + b, -1, tpd);
           } else {
             t_local = fmax(0.0, T - base);
           }
@@ -503,7 +523,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     if (mode == 0)
       mass_out[b] = samp.W;
     else
-      token_out[b] = idx < 0 ? -1 : p.vocab_offset + idx;
+      put_peers(token_out + b, idx < 0 ? -1 : p.vocab_offset + idx, tpd);
   }
 }
 
@@ -512,8 +532,12 @@ cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const doub
                                const int32_t *topi, int P, size_t rank_bytes, const void *draft,
                                const void *target, const int32_t *tokens, const DevOut &o,
                                int32_t *position, double *uniform, double *mass_out,
-                               double *tiles, cudaStream_t stream) {
-  if (P < 1 || P > kMaxShards || p.gamma > 31) return cudaErrorInvalidValue;
+                               double *tiles, cudaStream_t stream, const long long *mass_delta,
+                               int n_delta) {
+  if (P < 1 || P > kMaxShards || p.gamma > 31 || n_delta > 8) return cudaErrorInvalidValue;
+  PeerDelta mpd{};
+  mpd.n = n_delta;
+  for (int q = 0; q < n_delta; ++q) mpd.d[q] = mass_delta[q];
   const int G1 = p.gamma + 1;
   MergeIn in{rec, topv, topi, P, (size_t)p.B * G1 * kRecordWords,
              (size_t)p.B * p.gamma * 2 * p.top_m, (size_t)p.B * p.gamma * 2 * p.top_m};
@@ -526,11 +550,12 @@ cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const doub
   if (threads <= 320)
     shard_merge_kernel<In, 320, 4><<<p.B, threads, 0, stream>>>(p, in, (const In *)draft,
                                                                (const In *)target, tokens, o,
-                                                               position, uniform, mass_out, tiles);
+                                                               position, uniform, mass_out, tiles,
+                                                               mpd);
   else
     shard_merge_kernel<In><<<p.B, threads, 0, stream>>>(p, in, (const In *)draft,
                                                       (const In *)target, tokens, o, position,
-                                                      uniform, mass_out, tiles);
+                                                      uniform, mass_out, tiles, mpd);
   return cudaGetLastError();
 }
 
@@ -539,10 +564,15 @@ cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nran
                                 const void *draft, const void *target, const double *records,
                                 const int32_t *position, const double *uniform,
                                 const double *masses, double *mass_out, int32_t *token_out,
-                                int32_t *status, const double *tiles, cudaStream_t stream) {
+                                int32_t *status, const double *tiles, cudaStream_t stream,
+                                const long long *tok_delta, int n_delta, size_t mstride) {
+  if (n_delta > 8) return cudaErrorInvalidValue;
+  PeerDelta tpd{};
+  tpd.n = n_delta;
+  for (int q = 0; q < n_delta; ++q) tpd.d[q] = tok_delta[q];
   shard_sample_kernel<In><<<p.B, kConsumerThreads, 0, stream>>>(
       p, mode, rank, nranks, (const In *)draft, (const In *)target, records, position, uniform,
-      masses, mass_out, token_out, status, tiles);
+      masses, mass_out, token_out, status, tiles, tpd, mstride ? mstride : (size_t)p.B);
   return cudaGetLastError();
 }
 
@@ -550,7 +580,8 @@ cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nran
   template cudaError_t launch_shard_merge<T>(const DevParams &, const double *, const double *,  \
                                              const int32_t *, int, size_t, const void *,        \
                                              const void *, const int32_t *, const DevOut &,     \
-                                             int32_t *, double *, double *, double *, cudaStream_t);
+                                             int32_t *, double *, double *, double *, cudaStream_t, \
+                                             const long long *, int);
 DSDV_MERGE_INST(__nv_bfloat16)
 DSDV_MERGE_INST(float)
 DSDV_MERGE_INST(double)
@@ -560,16 +591,18 @@ template cudaError_t launch_shard_sample<__nv_bfloat16>(const DevParams &, int, 
                                                         const void *, const void *, const double *,
                                                         const int32_t *, const double *,
                                                         const double *, double *, int32_t *,
-                                                        int32_t *, const double *, cudaStream_t);
+                                                        int32_t *, const double *, cudaStream_t,
+                                                        const long long *, int, size_t);
 template cudaError_t launch_shard_sample<float>(const DevParams &, int, int, int, const void *,
                                                 const void *, const double *, const int32_t *,
                                                 const double *, const double *, double *,
-                                                int32_t *, int32_t *, const double *, cudaStream_t);
+                                                int32_t *, int32_t *, const double *, cudaStream_t,
+                                                const long long *, int, size_t);
 template cudaError_t launch_shard_sample<double>(const DevParams &, int, int, int, const void *,
                                                  const void *, const double *, const int32_t *,
                                                  const double *, const double *, double *,
                                                  int32_t *, int32_t *, const double *,
-                                                 cudaStream_t);
+                                                 cudaStream_t, const long long *, int, size_t);
 
 // ------------------------------------------------------------------ peer exchange
 struct PeerBases {
@@ -623,6 +656,22 @@ cudaError_t launch_peer_signal(char *const *bases, int nranks, int rank, unsigne
 cudaError_t launch_peer_wait(const unsigned long long *flags, int nranks, unsigned long long epoch,
                              unsigned long long timeout_ns, int *status, cudaStream_t stream) {
   peer_wait_kernel<<<1, 32, 0, stream>>>(flags, nranks, epoch, timeout_ns, status);
+  return cudaGetLastError();
+}
+
+// token[b] = max over ranks of their RESOLVE outputs (-1 where not the owner)
+__global__ void tokens_max_kernel(const int32_t *tok, size_t stride, int nranks, int B,
+                                  int32_t *out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int32_t m = -1;
+  for (int q = 0; q < nranks; ++q) m = max(m, tok[(size_t)q * stride + b]);
+  out[b] = m;
+}
+
+cudaError_t launch_tokens_max(const int32_t *tok, size_t stride, int nranks, int B, int32_t *out,
+                              cudaStream_t stream) {
+  tokens_max_kernel<<<(B + 255) / 256, 256, 0, stream>>>(tok, stride, nranks, B, out);
   return cudaGetLastError();
 }
 

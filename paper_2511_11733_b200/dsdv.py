@@ -99,6 +99,15 @@ def _load() -> C.CDLL:
                                         vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp]),
         "dsdv_peer_signal": (st, [vp, C.c_int32, C.c_int32, vp, C.c_uint64, C.c_uint64, vp]),
         "dsdv_peer_wait": (st, [vp, C.c_int32, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]),
+        "dsdv_shard_merge_peers": (st, [vp, C.POINTER(_Params), C.c_int32, C.c_int32, vp,
+                                        C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                        C.c_uint64, vp, vp, vp, C.POINTER(_Outputs), vp, vp, vp,
+                                        vp]),
+        "dsdv_shard_resolve_peers": (st, [vp, C.POINTER(_Params), C.c_int32, C.c_int32, vp,
+                                          C.c_uint64, C.c_uint64, C.c_uint64, vp, vp, vp, vp, vp,
+                                          vp, vp, vp]),
+        "dsdv_peer_tokens_max": (st, [vp, C.c_int32, vp, C.c_uint64, C.c_uint64, C.c_int32, vp,
+                                      vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -114,7 +123,8 @@ EXPORTED = ("dsdv_create", "dsdv_destroy", "dsdv_last_error", "dsdv_abi_version"
             "dsdv_shard_stats", "dsdv_shard_merge", "dsdv_shard_sample", "dsdv_mix_rows",
             "dsdv_spin", "dsdv_draft_sample_temperature", "dsdv_dev_alloc", "dsdv_dev_free",
             "dsdv_ipc_handle", "dsdv_ipc_open", "dsdv_ipc_close", "dsdv_shard_stats_peers",
-            "dsdv_peer_signal", "dsdv_peer_wait")
+            "dsdv_peer_signal", "dsdv_peer_wait", "dsdv_shard_merge_peers",
+            "dsdv_shard_resolve_peers", "dsdv_peer_tokens_max")
 
 
 def uniform(seed: int, window: int, sequence: int, slot: int) -> float:

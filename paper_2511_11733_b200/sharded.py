@@ -165,10 +165,26 @@ class ShardedVerifier:
                                            base + o_tv, base + o_ti, s))
         return buf
 
+    @staticmethod
+    def exchange_layout(B: int, G: int, M: int):
+        """One rank's slot in a peer-exchange set: the packed records, then its
+        [B] slice masses and [B] RESOLVE tokens. Returns (offsets, size)."""
+        (o_rec, o_tv, o_ti), size = ShardedVerifier.packed_layout(B, G, M)
+        o_mass = -(-size // 8) * 8
+        o_tok = o_mass + 8 * B
+        return (o_rec, o_tv, o_ti, o_mass, o_tok), o_tok + 4 * B
+
+    def signal_peers(self, ex: PeerExchange, value: int, stream=None, device=None):
+        s = (stream or torch.cuda.current_stream(device)).cuda_stream
+        flags = (C.c_void_p * ex.P)(*ex.flag_bases())
+        self.v._check(LIB.dsdv_peer_signal(self.v._h, ex.P, ex.rank, flags, ex.stride, value, s))
+
     def stats_peers(self, ex: PeerExchange, epoch: int, draft, target, tokens,
-                    p: VerifyParams, vocab: int, offset: int, local: int, stream=None):
+                    p: VerifyParams, vocab: int, offset: int, local: int, stream=None,
+                    flag: int | None = None):
         """dsdv_shard_stats_peers: this rank's records into every rank's buffer
-        set `epoch & 1`, then its arrival flag (epoch) in every rank's buffer."""
+        set `epoch & 1`, then its arrival flag (`flag`, default epoch) in every
+        rank's buffer."""
         B, G, _ = draft.shape
         M = min(p.top_m, vocab)
         cp = self._cp(p, draft, target, tokens, vocab, offset, local)
@@ -179,8 +195,52 @@ class ShardedVerifier:
         self.v._check(LIB.dsdv_shard_stats_peers(
             self.v._h, C.byref(cp), draft.data_ptr(), target.data_ptr(), tokens.data_ptr(), ex.P,
             ex.rank, bases, ex.stride, o_rec, o_tv, o_ti, s))
-        flags = (C.c_void_p * ex.P)(*ex.flag_bases())
-        self.v._check(LIB.dsdv_peer_signal(self.v._h, ex.P, ex.rank, flags, ex.stride, epoch, s))
+        self.signal_peers(ex, epoch if flag is None else flag, stream, draft.device)
+
+    def merge_peers(self, ex: PeerExchange, epoch: int, draft, target, tokens, p: VerifyParams,
+                    vocab: int, offset: int, local: int, out: WindowResult | None = None,
+                    stream=None):
+        """dsdv_shard_merge_peers: records from this rank's buffer set, the slice
+        masses stored into every rank's set. Returns (out, position, u)."""
+        B, G, _ = draft.shape
+        M = min(p.top_m, vocab)
+        cp = self._cp(p, draft, target, tokens, vocab, offset, local)
+        if out is None:
+            out = WindowResult.allocate(B, G, draft.device, True, records=True)
+        position = torch.empty(B, dtype=torch.int32, device=draft.device)
+        u = torch.empty(B, dtype=torch.float64, device=draft.device)
+        self._tiles = torch.empty((B, TILE_WORDS), dtype=torch.float64, device=draft.device)
+        (o_rec, o_tv, o_ti, o_mass, _), _ = self.exchange_layout(B, G, M)
+        s = (stream or torch.cuda.current_stream(draft.device)).cuda_stream
+        bases = (C.c_void_p * ex.P)(*ex.set_bases(epoch))
+        self.v._check(LIB.dsdv_shard_merge_peers(
+            self.v._h, C.byref(cp), ex.P, ex.rank, bases, ex.stride, o_rec, o_tv, o_ti, o_mass,
+            draft.data_ptr(), target.data_ptr(), tokens.data_ptr(), C.byref(out._c),
+            position.data_ptr(), u.data_ptr(), self._tiles.data_ptr(), s))
+        return out, position, u
+
+    def resolve_peers(self, ex: PeerExchange, epoch: int, draft, target, tokens,
+                      p: VerifyParams, vocab: int, offset: int, local: int, out: WindowResult,
+                      position, u, stream=None):
+        """dsdv_shard_resolve_peers: masses from this rank's set, tokens into
+        every rank's set."""
+        B, G, _ = draft.shape
+        cp = self._cp(p, draft, target, tokens, vocab, offset, local)
+        (_, _, _, o_mass, o_tok), _ = self.exchange_layout(B, G, min(p.top_m, vocab))
+        s = (stream or torch.cuda.current_stream(draft.device)).cuda_stream
+        bases = (C.c_void_p * ex.P)(*ex.set_bases(epoch))
+        self.v._check(LIB.dsdv_shard_resolve_peers(
+            self.v._h, C.byref(cp), ex.P, ex.rank, bases, ex.stride, o_mass, o_tok,
+            draft.data_ptr(), target.data_ptr(), out.records.data_ptr(), position.data_ptr(),
+            u.data_ptr(), out.status.data_ptr(), self._tiles.data_ptr(), s))
+
+    def tokens_max_peers(self, ex: PeerExchange, epoch: int, B: int, G: int, M: int,
+                         token_out: torch.Tensor, stream=None):
+        (_, _, _, _, o_tok), _ = self.exchange_layout(B, G, M)
+        s = (stream or torch.cuda.current_stream(token_out.device)).cuda_stream
+        local = ex.set_bases(epoch)[ex.rank]
+        self.v._check(LIB.dsdv_peer_tokens_max(self.v._h, ex.P, C.c_void_p(local), ex.stride,
+                                               o_tok, B, token_out.data_ptr(), s))
 
     def wait_peers(self, ex: PeerExchange, epoch: int, status: torch.Tensor, stream=None,
                    timeout_s: float = 10.0):
@@ -241,18 +301,30 @@ class ShardedVerifier:
         """One window on this rank. exchange="peer": the records travel by the
         stats kernel's own NVLink stores (PeerExchange) instead of an all-gather."""
         if exchange == "peer":
+            # no collective call: three flag rounds over the mapped buffers
             B, G, _ = draft.shape
-            _, size = self.packed_layout(B, G, min(p.top_m, vocab))
+            M = min(p.top_m, vocab)
+            _, size = self.exchange_layout(B, G, M)
             ex = getattr(self, "_ex", None)
             if ex is None or ex.stride < size:
                 ex = self._ex = PeerExchange(self.v, comm.size, comm.rank, size, comm=comm)
                 self._epoch = 0
                 self._peer_status = torch.zeros(1, dtype=torch.int32, device=draft.device)
             self._epoch += 1
-            self.stats_peers(ex, self._epoch, draft, target, tokens, p, vocab, offset, local,
-                             stream)
-            self.wait_peers(ex, self._epoch, self._peer_status, stream)
-            merged_in = (ex.set_bases(self._epoch)[ex.rank], ex.P, ex.stride)
+            w, f = self._epoch, 3 * self._epoch
+            self.stats_peers(ex, w, draft, target, tokens, p, vocab, offset, local, stream,
+                             flag=f)
+            self.wait_peers(ex, f, self._peer_status, stream)
+            out, position, u = self.merge_peers(ex, w, draft, target, tokens, p, vocab, offset,
+                                                local, out, stream)
+            self.signal_peers(ex, f + 1, stream, draft.device)
+            self.wait_peers(ex, f + 1, self._peer_status, stream)
+            self.resolve_peers(ex, w, draft, target, tokens, p, vocab, offset, local, out,
+                               position, u, stream)
+            self.signal_peers(ex, f + 2, stream, draft.device)
+            self.wait_peers(ex, f + 2, self._peer_status, stream)
+            self.tokens_max_peers(ex, w, B, G, M, out.extra_token, stream)
+            return out
         else:
             packed = self.stats(draft, target, tokens, p, vocab, offset, local, stream)
             merged_in = comm.all_gather(packed)
@@ -279,11 +351,13 @@ def contiguous_slice(rows: torch.Tensor, lo: int, n: int) -> torch.Tensor:
 def shard_slices_peer(verifier: Verifier, draft: torch.Tensor, target: torch.Tensor,
                       tokens: torch.Tensor, p: VerifyParams, vocab: int, nranks: int,
                       epoch: int = 1) -> WindowResult:
-    """shard_slices with the peer exchange: every virtual rank's stats pass
-    stores its records into all P exchange buffers (plain device buffers of this
-    process instead of IPC mappings), flags arrive, each rank merges its own."""
+    """shard_slices with the peer exchange (the collective-free window of
+    ShardedVerifier.verify(exchange="peer")): every virtual rank stores into all
+    P exchange buffers — plain device buffers of this process instead of IPC
+    mappings — with the same three flag rounds."""
     B, G, _ = draft.shape
-    _, size = ShardedVerifier.packed_layout(B, G, min(p.top_m, vocab))
+    M = min(p.top_m, vocab)
+    _, size = ShardedVerifier.exchange_layout(B, G, M)
     bases = PeerExchange.allocate_local(verifier, nranks, size)
     exs = [PeerExchange(verifier, nranks, r, size, bases=bases) for r in range(nranks)]
     svs = [ShardedVerifier(verifier) for _ in range(nranks)]
@@ -291,25 +365,31 @@ def shard_slices_peer(verifier: Verifier, draft: torch.Tensor, target: torch.Ten
     for r in range(nranks):
         lo, n = slice_bounds(vocab, nranks, r)
         parts.append((lo, n, contiguous_slice(draft, lo, n), contiguous_slice(target, lo, n)))
-    for r, (lo, n, d, t) in enumerate(parts):
-        svs[r].stats_peers(exs[r], epoch, d, t, tokens, p, vocab, lo, n)
     status = torch.zeros(1, dtype=torch.int32, device=draft.device)
+    f = 3 * epoch
+    for r, (lo, n, d, t) in enumerate(parts):
+        svs[r].stats_peers(exs[r], epoch, d, t, tokens, p, vocab, lo, n, flag=f)
     merged = []
     for r, (lo, n, d, t) in enumerate(parts):
-        svs[r].wait_peers(exs[r], epoch, status, timeout_s=2.0)
-        merged.append(svs[r].merge(d, t, tokens, p, vocab, lo, n,
-                                   (exs[r].set_bases(epoch)[r], nranks, exs[r].stride)))
-    masses = torch.stack([m[3] for m in merged])
-    toks = torch.stack([svs[r].sample(SHARD_RESOLVE, r, nranks, d, t, tokens, p, vocab, lo, n,
-                                      *merged[r][:3], masses, tiles=svs[r]._tiles)
-                        for r, (lo, n, d, t) in enumerate(parts)])
-    out = merged[0][0]
-    out.extra_token.copy_(toks.max(dim=0).values)
+        svs[r].wait_peers(exs[r], f, status, timeout_s=2.0)
+        merged.append(svs[r].merge_peers(exs[r], epoch, d, t, tokens, p, vocab, lo, n))
+        svs[r].signal_peers(exs[r], f + 1, device=draft.device)
+    for r, (lo, n, d, t) in enumerate(parts):
+        svs[r].wait_peers(exs[r], f + 1, status, timeout_s=2.0)
+        out, position, u = merged[r]
+        svs[r].resolve_peers(exs[r], epoch, d, t, tokens, p, vocab, lo, n, out, position, u)
+        svs[r].signal_peers(exs[r], f + 2, device=draft.device)
+    for r in range(nranks):
+        svs[r].wait_peers(exs[r], f + 2, status, timeout_s=2.0)
+        svs[r].tokens_max_peers(exs[r], epoch, B, G, M, merged[r][0].extra_token)
     torch.cuda.synchronize(draft.device)
     assert int(status.item()) == 0, "peer wait timed out"
+    for r in range(1, nranks):  # every rank holds the same window
+        for k in ("accepted_count", "extra_token", "key_count", "status"):
+            assert torch.equal(getattr(merged[r][0], k), getattr(merged[0][0], k)), k
     for b in bases:
         LIB.dsdv_dev_free(verifier._h, C.c_void_p(b))
-    return out
+    return merged[0][0]
 
 
 def shard_slices(verifier: Verifier, draft: torch.Tensor, target: torch.Tensor,
