@@ -409,9 +409,9 @@ def run_sharded(args, rank, world, local_rank):
                                f"({n} ids on rank 0), B={Bt} (256 per GPU), gamma=8, bf16 logits, "
                                "tau=0.2, lambda=(2.0, 0.2, 0.5), top_m=10",
                    "batch_total": Bt, "gamma": GAMMA, "vocab": V, "vocab_per_rank": n,
-                   "parallelism": (f"vocab-sharded tp{world} (records: fused NVLink peer "
-                                   "stores from the stats kernel + flags; NCCL: 1 all-gather "
-                                   "of [B] masses + 1 all-reduce per window)")
+                   "parallelism": (f"vocab-sharded tp{world} (no collective call per window: "
+                                   "records, masses and tokens as the kernels' NVLink peer "
+                                   "stores into IPC-mapped buffers + flag rounds)")
                    if args.exchange == "peer" else
                    (f"vocab-sharded tp{world} (NCCL: 2 all-gathers + 1 all-reduce "
                     "per window)"),
