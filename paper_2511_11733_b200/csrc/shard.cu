@@ -96,18 +96,22 @@ __global__ void __launch_bounds__(MAXT, MINB)
     int f = 0;
     for (int q = lane; q < in.P; q += 32) {
       const double *r = in.rec + q * in.rec_stride + ((size_t)b * G1 + j) * kRecordWords;
+      // running log-sum-exp over this lane's slices (the first one is exact:
+      // log(0 + e^0) = 0, so it is taken as is, without the transcendentals)
+      auto lse2 = [](double acc, double a) -> double {
+        if (acc == -INFINITY) return a;
+        const double m = fmax(acc, a);
+        return m == -INFINITY ? -(double)INFINITY : m + log(exp(acc - m) + exp(a - m));
+      };
       const double a_t = r[0] + r[1];
       if (a_t > -INFINITY) mtq = fmax(mtq, r[0]);
-      double m = fmax(lt, a_t);
-      lt = (m == -INFINITY) ? -INFINITY : m + log(exp(lt - m) + exp(a_t - m));
+      lt = lse2(lt, a_t);
       if (pair) {
         const double a_d = r[2] + r[3];
         if (a_d > -INFINITY) mdq = fmax(mdq, r[2]);
-        m = fmax(ld, a_d);
-        ld = (m == -INFINITY) ? -INFINITY : m + log(exp(ld - m) + exp(a_d - m));
+        ld = lse2(ld, a_d);
         const double a_z = omt * r[0] + tau * r[2] + r[4];
-        m = fmax(lz, a_z);
-        lz = (m == -INFINITY) ? -INFINITY : m + log(exp(lz - m) + exp(a_z - m));
+        lz = lse2(lz, a_z);
         const int fl = (int)r[7];
         f |= fl;
         if (fl & 2) {

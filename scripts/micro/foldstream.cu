@@ -124,6 +124,36 @@ __global__ void __launch_bounds__(17 * 32, 1)
   if (S.st == 12345.f) sink[0] = S.st + S.sd + S.sz;
   return;
 #endif
+#if PAIRWAIT
+  // two stages per synchronisation: wait for both, fold both, release both
+  for (;;) {
+    const int st2 = st + 1 == stages ? 0 : st + 1;
+    const uint32_t ph2 = st + 1 == stages ? ph ^ 1 : ph;
+    wait(&full[st], ph);
+    if (chunk_of[st] < 0) break;
+    wait(&full[st2], ph2);
+    const bool second = chunk_of[st2] >= 0;
+    fold_chunk<__nv_bfloat16, true, true, false>(sm + (size_t)st * SB, sm + (size_t)st * SB + SB / 2,
+                                                threadIdx.x, 8 + (int)(chunk_of[st] & 7), S, cp, warp, lane,
+                                                *sl, bmt, bmd, nullptr);
+    if (second)
+      fold_chunk<__nv_bfloat16, true, true, false>(sm + (size_t)st2 * SB, sm + (size_t)st2 * SB + SB / 2,
+                                                  threadIdx.x, 8 + (int)(chunk_of[st2] & 7), S, cp, warp, lane,
+                                                  *sl, bmt, bmd, nullptr);
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[st])) : "memory");
+      if (second) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[st2])) : "memory");
+    }
+    if (!second) break;
+    st = st2 + 1 == stages ? 0 : st2 + 1;
+    if (st2 + 1 == stages || st + 0 == 0 && st2 != stages - 1) {}
+    // phase flips whenever the index wraps
+    if (st == 0 || st2 == 0) ph ^= 1;
+  }
+  if (S.st == 12345.f) sink[0] = S.st + S.sd + S.sz;
+  return;
+#endif
   for (;;) {
 #if CONSHINT
     wait_hint(&full[st], ph);
@@ -164,7 +194,7 @@ int main() {
   const int works[] = {0, 1};
   for (int vary : {0})
   for (int rowwise : {2})
-  for (int stages : {5}) {
+  for (int stages : {STAGES}) {
     const size_t smem = (size_t)32768 * stages + 1024;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int w : works) {
