@@ -37,9 +37,22 @@ if os.environ.get("NONEKEY"):
     p.ratio_limit, p.gap_limit, p.overlap_floor = float("inf"), 1.0, 0.0
 tokens = v.draft_sample(draft, p, vocab=V)
 out = WindowResult.allocate(B, G, draft.device, per_position=False)
+SHARD = int(os.environ.get("SHARD", 0))  # >0: the partial stats pass of slice 0 of SHARD
+if SHARD:
+    from paper_2511_11733_b200.sharded import ShardedVerifier, contiguous_slice, slice_bounds
+    sv = ShardedVerifier(v)
+    lo, n = slice_bounds(V, SHARD, 0)
+    ds, ts = contiguous_slice(draft, lo, n), contiguous_slice(target, lo, n)
+
+
+def run_window():
+    if SHARD:
+        sv.stats(ds, ts, tokens, p, V, lo, n)
+    else:
+        run_window()
 for w in range(3):
     p.window = w
-    v.verify(draft, target, tokens, p, vocab=V, out=out)
+    run_window()
 torch.cuda.synchronize()
 buf = np.zeros((1024, 28), dtype=np.uint64)
 lib.dsdv_debug_trace(v._h, buf.ctypes.data, 1024)  # clear
@@ -48,7 +61,7 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 e0.record()
 for w in range(reps):
     p.window = 100 + w
-    v.verify(draft, target, tokens, p, vocab=V, out=out)
+    run_window()
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
