@@ -112,3 +112,27 @@ def test_slice_bounds_cover_the_vocabulary():
             assert sum(n for _, n in parts) == V
             for (lo, n), (lo2, _) in zip(parts, parts[1:]):
                 assert lo + n == lo2 and lo2 % 8 == 0
+
+
+def test_peer_exchange_layout():
+    """Slot layout of the collective-free window: records, top lists, masses and
+    tokens aligned for their element types and inside one stride; the flag array
+    sits after both alternating sets (host arithmetic only, no device)."""
+    from paper_2511_11733_b200.sharded import PeerExchange, ShardedVerifier
+    for B, G, M in ((256, 8, 10), (1024, 16, 6), (3, 1, 1)):
+        (o_rec, o_tv, o_ti, o_mass, o_tok), size = ShardedVerifier.exchange_layout(B, G, M)
+        (p_rec, p_tv, p_ti), psize = ShardedVerifier.packed_layout(B, G, M)
+        assert (o_rec, o_tv, o_ti) == (p_rec, p_tv, p_ti)
+        assert o_mass >= psize and o_mass % 8 == 0 and o_tok == o_mass + 8 * B
+        assert size == o_tok + 4 * B
+        for P in (2, 4, 8):
+            bases = [(q + 1) << 32 for q in range(P)]
+            ex = PeerExchange(None, P, P - 1, size, bases=bases)
+            assert ex.stride >= size and ex.stride % 256 == 0
+            for w in (1, 2):
+                sets = ex.set_bases(w)
+                assert [s - b for s, b in zip(sets, bases)] == [(w & 1) * P * ex.stride] * P
+            # dsdv_peer_signal / _wait address flag q at flag_base + P * stride + 8 q
+            assert [f + P * ex.stride - b for f, b in zip(ex.flag_bases(), bases)] == \
+                [2 * P * ex.stride] * P
+            assert ex.bytes == 2 * P * ex.stride + 8 * P
