@@ -69,3 +69,23 @@ def test_peer_exchange_equals_gathered(verifier, oracle, P):
                                          torch.equal(a.nan_to_num(7.0), b.nan_to_num(7.0))), k
     rep = compare_window(oracle, d64, t64, toks, got, 0.2, crit, 3, 0)
     assert rep.ok(), rep.mismatches[:5]
+
+
+def test_peer_exchange_across_processes():
+    """The real thing when the box has two GPUs: torchrun, CUDA IPC mappings,
+    NVLink peer stores and flag rounds, compared with the NCCL path on every
+    rank over several windows (scripts/peer_check.py)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29561",
+           str(root / "scripts" / "peer_check.py")]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "OMP_NUM_THREADS": "1"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "OK (0 differing fields" in r.stdout, r.stdout[-2000:]
