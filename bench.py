@@ -415,7 +415,8 @@ def run_sharded(args, rank, world, local_rank):
                    if args.exchange == "peer" else
                    (f"vocab-sharded tp{world} (NCCL: 2 all-gathers + 1 all-reduce "
                     "per window)"),
-                   "exchange": args.exchange,
+                   "exchange": ("nccl (peer mapping unavailable)"
+                                if getattr(sv, "peer_fallback", False) else args.exchange),
                    "l2": "no flush needed: 1.12 GB of logits per GPU per step > 126 MB L2",
                    "mean_accepted_k": mean_k, "status_errors": bad,
                    "host_enqueue_ms_per_step": host_ms,

@@ -300,6 +300,8 @@ class ShardedVerifier:
                exchange: str = "nccl") -> WindowResult:
         """One window on this rank. exchange="peer": the records travel by the
         stats kernel's own NVLink stores (PeerExchange) instead of an all-gather."""
+        if exchange == "peer" and getattr(self, "peer_fallback", False):
+            exchange = "nccl"
         if exchange == "peer":
             # no collective call: three flag rounds over the mapped buffers
             B, G, _ = draft.shape
@@ -307,7 +309,21 @@ class ShardedVerifier:
             _, size = self.exchange_layout(B, G, M)
             ex = getattr(self, "_ex", None)
             if ex is None or ex.stride < size:
-                ex = self._ex = PeerExchange(self.v, comm.size, comm.rank, size, comm=comm)
+                # collective setup; if any rank cannot map its peers (no CUDA IPC
+                # / peer access), every rank falls back to the NCCL exchange
+                try:
+                    ex = PeerExchange(self.v, comm.size, comm.rank, size, comm=comm)
+                    ok = 1
+                except Exception:  # noqa: BLE001  (reported through the flag)
+                    ex, ok = None, 0
+                flags = comm.all_gather(torch.tensor([ok], dtype=torch.int32, device=draft.device))
+                if int(flags.min().item()) == 0:
+                    if ex is not None:
+                        ex.close()
+                    self.peer_fallback = True
+                    return self.verify(draft, target, tokens, p, vocab, offset, local, comm, out,
+                                       stream, exchange="nccl")
+                self._ex = ex
                 self._epoch = 0
                 self._peer_status = torch.zeros(1, dtype=torch.int32, device=draft.device)
             self._epoch += 1
