@@ -835,7 +835,11 @@ __device__ __noinline__ void select_topm(Slot<typename InTraits<In>::Acc> &sl, i
   return;  // development probe: capture off (results are wrong)
 #endif
   // the final bins hold every block's lane maxima: the tightest bound
-  const int th = max(vload(&sl.ktheta[r]), theta_from_bins(sl.klist[r], M, lane));
+  int th = max(vload(&sl.ktheta[r]), theta_from_bins(sl.klist[r], M, lane));
+  // short rows (vocabulary slices): the M-th largest block maximum of each group
+  // of 32 blocks is a valid bound too and usually tighter -> fewer survivors
+  if (nblocks <= 64 && nblocks % 32 == 0)
+    for (int g = 0; g < nblocks; g += 32) th = max(th, theta_from_bins(bmax + g, M, lane));
   const int ncap = vload(&sl.ncap[r]);
   TR_ACC(trl, kTrTopmCand, ncap);
   if (ncap <= kCap) {
