@@ -309,6 +309,10 @@ class ShardedVerifier:
             _, size = self.exchange_layout(B, G, M)
             ex = getattr(self, "_ex", None)
             if ex is None or ex.stride < size:
+                if ex is not None:  # a larger window: remap (every rank does the same)
+                    torch.cuda.synchronize(draft.device)
+                    ex.close()
+                    self._ex = None
                 # collective setup; if any rank cannot map its peers (no CUDA IPC
                 # / peer access), every rank falls back to the NCCL exchange
                 try:
