@@ -89,3 +89,23 @@ def test_peer_exchange_across_processes():
                        env={**os.environ, "OMP_NUM_THREADS": "1"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert "OK (0 differing fields" in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("dtype,P,tau", [(torch.float32, 3, 0.5), (torch.bfloat16, 4, 1.0),
+                                         (torch.float32, 2, 0.0)])
+def test_peer_exchange_dtypes(verifier, oracle, dtype, P, tau):
+    """The collective-free window for fp32 slices, odd P and the τ endpoints,
+    bit-equal to the gathered window and parity-green against the oracle."""
+    from paper_2511_11733_b200.sharded import shard_slices_peer
+    crit = Oracle.crit(2.0, 0.2, 0.5, 6)
+    V = 5000
+    d64, t64, toks, unsharded, (draft, target, tokens, p) = run_gpu_window(
+        verifier, dtype, 8, 4, V, tau, crit, seed=11, oracle=oracle)
+    ref = shard_slices(verifier, draft, target, tokens, p, V, P).to_host()
+    got = shard_slices_peer(verifier, draft, target, tokens, p, V, P, epoch=2).to_host()
+    for k in ref:
+        a, b = torch.as_tensor(got[k]), torch.as_tensor(ref[k])
+        assert torch.equal(a, b) or (a.is_floating_point() and
+                                     torch.equal(a.nan_to_num(7.0), b.nan_to_num(7.0))), k
+    rep = compare_window(oracle, d64, t64, toks, got, tau, crit, 11, 0)
+    assert rep.ok(), rep.mismatches[:5]
