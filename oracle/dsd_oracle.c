@@ -419,3 +419,141 @@ int oracle_verify_batch_f32(int B, int gamma, int V, int stride, const float *dr
   free(jobs);
   return 0;
 }
+
+/* ---- parity checker: B windows x ncfg (tau, criteria) configurations ---- */
+
+static double bf16_to_double(uint16_t h) {
+  union {
+    uint32_t u;
+    float f;
+  } v;
+  v.u = (uint32_t)h << 16;
+  return (double)v.f;
+}
+
+static void row_to_f64(const void *base, int dtype, size_t row, int stride, int V, double *out) {
+  if (dtype == 1) {
+    const uint16_t *r = (const uint16_t *)base + row * (size_t)stride;
+    for (int i = 0; i < V; ++i) out[i] = bf16_to_double(r[i]);
+  } else {
+    const float *r = (const float *)base + row * (size_t)stride;
+    for (int i = 0; i < V; ++i) out[i] = (double)r[i];
+  }
+}
+
+typedef struct {
+  int B, gamma, V, stride, dtype, ncfg, all_positions, nthreads, tid;
+  const void *draft, *target;
+  const int32_t *tokens;
+  const double *taus;
+  const oracle_criteria *crits;
+  const double *uniforms;
+  oracle_batch_out *outs;
+} full_job;
+
+/* Per-position quantities of verify_round (verifier.cpp:223-236) without the
+ * draw: for positions after the first rejection, which the reference never
+ * evaluates but the device computes (numerics only). */
+static void position_numerics(const double *pt, const double *pd, int V, int y, double tau,
+                              const oracle_criteria *c, double *eff, oracle_batch_out *o,
+                              size_t pos) {
+  if (y < 0 || y >= V) return;
+  double km[2];
+  const int key = oracle_is_key(pt, pd, V, y, c, km);
+  if (key)
+    memcpy(eff, pt, sizeof(double) * (size_t)V);
+  else if (oracle_soften(pt, pd, V, tau, eff) != ORACLE_OK)
+    return;
+  int err = 0;
+  const double a = oracle_accept_prob(eff, pd, y, &err);
+  const int m = c->top_m < V ? c->top_m : V;
+  o->key[pos] = (uint8_t)key;
+  o->accept_prob[pos] = err ? NAN : a;
+  o->h_target[pos] = oracle_cross_entropy(pt, V, y);
+  o->h_draft[pos] = oracle_cross_entropy(pd, V, y);
+  o->p_target_y[pos] = pt[y];
+  o->p_draft_y[pos] = pd[y];
+  o->norm_match[pos] = oracle_norm_match(pt, pd, V, m);
+  o->p_eff_y[pos] = eff[y];
+  o->margin_key[pos] = km[0] < km[1] ? km[0] : km[1];
+}
+
+static void *full_worker(void *arg) {
+  full_job *j = (full_job *)arg;
+  const int G = j->gamma, V = j->V;
+  double *raw = (double *)malloc(sizeof(double) * (size_t)V);
+  double *pd = (double *)malloc(sizeof(double) * (size_t)G * V);
+  double *pt = (double *)malloc(sizeof(double) * (size_t)(G + 1) * V);
+  double *eff = (double *)malloc(sizeof(double) * (size_t)V);
+  int *row_err = (int *)malloc(sizeof(int) * (size_t)(2 * G + 1));
+  for (int b = j->tid; b < j->B; b += j->nthreads) {
+    for (int r = 0; r < G; ++r) {
+      row_to_f64(j->draft, j->dtype, (size_t)b * G + r, j->stride, V, raw);
+      row_err[r] = oracle_softmax(raw, V, pd + (size_t)r * V);
+    }
+    for (int r = 0; r <= G; ++r) {
+      row_to_f64(j->target, j->dtype, (size_t)b * (G + 1) + r, j->stride, V, raw);
+      row_err[G + r] = oracle_softmax(raw, V, pt + (size_t)r * V);
+    }
+    const int32_t *tok = j->tokens + (size_t)b * G;
+    for (int c = 0; c < j->ncfg; ++c) {
+      oracle_batch_out *o = &j->outs[c];
+      const size_t p0 = (size_t)b * G;
+      oracle_result r;
+      memset(&r, 0, sizeof(r));
+      r.key = o->key + p0;
+      r.accepted = o->accepted + p0;
+      r.accept_prob = o->accept_prob + p0;
+      r.h_target = o->h_target + p0;
+      r.h_draft = o->h_draft + p0;
+      r.p_target_y = o->p_target_y + p0;
+      r.p_draft_y = o->p_draft_y + p0;
+      r.norm_match = o->norm_match + p0;
+      r.p_eff_y = o->p_eff_y + p0;
+      r.margin_u = o->margin_u + p0;
+      r.margin_key = o->margin_key + p0;
+      oracle_slot_stream ss = {j->uniforms + (size_t)b * (2 * G + 1), G};
+      oracle_window w = {G,   V,         pd,   pt, row_err, tok, j->taus[c], j->crits[c],
+                         oracle_slot_next, &ss};
+      oracle_verify_window(&w, &r);
+      o->k[b] = r.accepted_count;
+      o->extra_token[b] = r.extra_token;
+      o->extra_source[b] = r.extra_source;
+      o->key_count[b] = r.key_count;
+      o->status[b] = r.status;
+      o->evaluated[b] = r.evaluated;
+      o->margin_extra[b] = r.margin_extra;
+      if (j->all_positions)
+        for (int q = r.evaluated; q < G; ++q)
+          if (!row_err[q] && !row_err[G + q])
+            position_numerics(pt + (size_t)q * V, pd + (size_t)q * V, V, tok[q], j->taus[c],
+                              &j->crits[c], eff, o, p0 + (size_t)q);
+    }
+  }
+  free(raw);
+  free(pd);
+  free(pt);
+  free(eff);
+  free(row_err);
+  return NULL;
+}
+
+int oracle_verify_batch(int B, int gamma, int V, int stride, int dtype, const void *draft,
+                        const void *target, const int32_t *tokens, int ncfg, const double *taus,
+                        const oracle_criteria *crits, const double *uniforms, int all_positions,
+                        int nthreads, oracle_batch_out *outs) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > B) nthreads = B;
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  full_job *jobs = (full_job *)malloc(sizeof(full_job) * (size_t)nthreads);
+  for (int t = 0; t < nthreads; ++t) {
+    full_job j = {B,      gamma,  V,        stride, dtype, ncfg, all_positions, nthreads, t,
+                  draft,  target, tokens,   taus,   crits, uniforms, outs};
+    jobs[t] = j;
+    pthread_create(&th[t], NULL, full_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  free(th);
+  free(jobs);
+  return 0;
+}

@@ -115,6 +115,24 @@ int oracle_verify_batch_f32(int B, int gamma, int V, int stride, const float *dr
                             const oracle_criteria *crit, const double *uniforms /*[B][2g+1]*/,
                             int nthreads, int32_t *k_out, int32_t *extra_out, int32_t *status_out);
 
+/* Parity checker: B windows over raw logits (dtype 0 = fp32, 1 = bf16 bits)
+ * for ncfg (tau, criteria) configurations, nthreads POSIX threads; rows are
+ * softmaxed once per sequence and shared by the configurations. Every output
+ * array is caller-owned: per sequence [B], per position [B][gamma]. Positions
+ * after the first rejection get the numerics (no draw) when all_positions. */
+typedef struct {
+  int32_t *k, *extra_token, *extra_source, *key_count, *status, *evaluated;
+  double *margin_extra;
+  uint8_t *key, *accepted;
+  double *accept_prob, *h_target, *h_draft, *p_target_y, *p_draft_y, *norm_match, *p_eff_y,
+      *margin_u, *margin_key;
+} oracle_batch_out;
+
+int oracle_verify_batch(int B, int gamma, int V, int stride, int dtype, const void *draft,
+                        const void *target, const int32_t *tokens, int ncfg, const double *taus,
+                        const oracle_criteria *crits, const double *uniforms /*[B][2g+1]*/,
+                        int all_positions, int nthreads, oracle_batch_out *outs /*[ncfg]*/);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,17 @@ class _Result(C.Structure):
                 ("margin_extra", C.c_double)]
 
 
+class _BatchOut(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in (
+        "k", "extra_token", "extra_source", "key_count", "status", "evaluated", "margin_extra",
+        "key", "accepted", "accept_prob", "h_target", "h_draft", "p_target_y", "p_draft_y",
+        "norm_match", "p_eff_y", "margin_u", "margin_key")]
+
+
+_BATCH_SEQ_I32 = ("k", "extra_token", "extra_source", "key_count", "status", "evaluated")
+_BATCH_POS_F64 = ("accept_prob", "h_target", "h_draft", "p_target_y", "p_draft_y", "norm_match",
+                  "p_eff_y", "margin_u", "margin_key")
+
 _PER_POS_U8 = ("key", "accepted")
 _PER_POS_F64 = ("accept_prob", "h_target", "h_draft", "p_target_y", "p_draft_y", "norm_match",
                 "p_eff_y", "uniform", "margin_u", "margin_key")
@@ -124,6 +135,9 @@ class Oracle:
         L.oracle_verify_batch_f32.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _fp, _fp, _ip,
                                               C.c_double, C.POINTER(_Crit), _dp, C.c_int, _ip,
                                               _ip, _ip]
+        L.oracle_verify_batch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                          C.c_void_p, _ip, C.c_int, _dp, C.c_void_p, _dp, C.c_int,
+                                          C.c_int, C.c_void_p]
         self.L = L
 
     @staticmethod
@@ -172,6 +186,12 @@ class Oracle:
         p = np.ascontiguousarray(p, dtype=np.float64)
         return self.L.oracle_sample_with_uniform(p, p.size, u, None)
 
+    def sample_with_margin(self, p, u) -> tuple[int, float]:
+        """sample_with_uniform plus the CDF margin |u - nearest boundary|."""
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        m = C.c_double(0.0)
+        return self.L.oracle_sample_with_uniform(p, p.size, u, C.byref(m)), m.value
+
     def verify_window(self, draft_logits, target_logits, tokens, tau, crit: _Crit,
                       uniforms) -> dict:
         """One sequence: draft [gamma][V], target [gamma+1][V] (fp64 copies)."""
@@ -209,6 +229,44 @@ class Oracle:
         if n < 0:
             raise RuntimeError(f"oracle_generate_iid failed with status {-n}")
         return ks[:n].tolist()
+
+    def verify_batch(self, draft, target, tokens, configs, uniforms, V, all_positions=False,
+                     nthreads=None) -> list[dict]:
+        """Parity checker over a whole batch: draft [B][gamma][stride],
+        target [B][gamma+1][stride] as fp32 or raw bf16 bits (uint16);
+        configs = [(tau, crit), ...] share the softmaxed rows. Returns one dict
+        of numpy arrays per configuration (per sequence [B], per position
+        [B][gamma]; NaN / 0 where the reference never evaluates)."""
+        if draft.dtype == np.uint16:
+            dtype = 1
+        else:
+            draft = draft.astype(np.float32, copy=False)
+            target = target.astype(np.float32, copy=False)
+            dtype = 0
+        draft = np.ascontiguousarray(draft)
+        target = np.ascontiguousarray(target)
+        B, G, stride = draft.shape
+        assert target.shape == (B, G + 1, stride)
+        tok = np.ascontiguousarray(tokens, dtype=np.int32).reshape(B, G)
+        U = np.ascontiguousarray(uniforms, dtype=np.float64).reshape(B, 2 * G + 1)
+        n = len(configs)
+        taus = np.ascontiguousarray([float(t) for t, _ in configs], dtype=np.float64)
+        crits = (_Crit * n)(*[c for _, c in configs])
+        res, outs = [], (_BatchOut * n)()
+        for i in range(n):
+            d = {k: np.zeros(B, np.int32) for k in _BATCH_SEQ_I32}
+            d["margin_extra"] = np.full(B, np.inf)
+            d["key"] = np.zeros((B, G), np.uint8)
+            d["accepted"] = np.zeros((B, G), np.uint8)
+            d.update({k: np.full((B, G), np.nan) for k in _BATCH_POS_F64})
+            for k, a in d.items():
+                setattr(outs[i], k, a.ctypes.data)
+            res.append(d)
+        self.L.oracle_verify_batch(B, G, V, stride, dtype, draft.ctypes.data, target.ctypes.data,
+                                   tok, n, taus, C.cast(crits, C.c_void_p), U,
+                                   1 if all_positions else 0, nthreads or os.cpu_count() or 1,
+                                   C.cast(outs, C.c_void_p))
+        return res
 
     def verify_batch_f32(self, draft, target, tokens, tau, crit: _Crit, uniforms, V,
                          nthreads=None):

@@ -164,6 +164,129 @@ def compare_window(oracle: Oracle, draft64, target64, tokens, gpu: dict, tau: fl
     return rep
 
 
+def _close_arr(g, r, rel, ab):
+    """Elementwise _close over arrays (inf only matches inf)."""
+    g = np.asarray(g, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    inf = np.isinf(g) | np.isinf(r)
+    with np.errstate(invalid="ignore"):
+        fin = np.abs(g - r) <= rel * np.abs(r) + ab
+    return np.where(inf, np.isinf(g) & np.isinf(r) & (np.sign(g) == np.sign(r)), fin)
+
+
+def _to_np(x):
+    return x.numpy() if hasattr(x, "numpy") else np.asarray(x)
+
+
+def compare_batch(ref: dict, gpu: dict, all_positions: bool = True,
+                  max_report: int = 50) -> ParityReport:
+    """compare_window over a whole batch against Oracle.verify_batch output
+    (one configuration). Same contract: numerics within tolerance at every
+    position the oracle evaluated (and at the later ones when it supplied
+    them), decisions bit-exact up to the first divergence, which must be an
+    epsilon event (oracle margin inside the band) to be excused."""
+    g = {k: _to_np(v) for k, v in gpu.items()}
+    B, G = ref["key"].shape
+    rep = ParityReport(sequences=B)
+    rep.ks = ref["k"].tolist()
+    rs, gs = ref["status"], g["status"].astype(np.int64)
+    bad_status = rs != gs
+    for b in np.nonzero(bad_status)[0][:max_report]:
+        rep.mismatches.append((int(b), "status", int(gs[b]), int(rs[b])))
+    ok_seq = (rs == 0) & (gs == 0)
+    ev = ref["evaluated"]
+    jj = np.arange(G)[None, :]
+    # positions with oracle numerics: evaluated ones (+ later ones with a finite h)
+    has = (jj < ev[:, None]) | (all_positions & ~np.isnan(ref["h_target"]))
+    has &= ok_seq[:, None]
+    rep.positions_checked = int(has.sum())
+
+    def check(name, gname, rel, ab, mask=None):
+        m = has if mask is None else (has & mask)
+        okv = _close_arr(g[gname], ref[name], rel, ab) | ~m
+        for b, j in zip(*np.nonzero(~okv)):
+            if len(rep.mismatches) < max_report:
+                rep.mismatches.append((int(b), int(j), name, float(g[gname][b, j]),
+                                       float(ref[name][b, j])))
+        return okv
+
+    check("h_target", "h_target", H_REL, H_ABS)
+    check("h_draft", "h_draft", H_REL, H_ABS)
+    check("p_target_y", "p_target_y", P_REL, P_ABS)
+    check("p_draft_y", "p_draft_y", P_REL, P_ABS)
+    nm_bad = has & (g["norm_match"] != ref["norm_match"])
+    for b, j in zip(*np.nonzero(nm_bad)):
+        if len(rep.mismatches) < max_report:
+            rep.mismatches.append((int(b), int(j), "norm_match", float(g["norm_match"][b, j]),
+                                   float(ref["norm_match"][b, j])))
+    same_key = g["key_mask"].astype(bool) == ref["key"].astype(bool)
+    check("p_eff_y", "p_effective_y", P_REL, P_ABS, same_key)
+    check("accept_prob", "accept_prob", P_REL, P_ABS, same_key)
+    with np.errstate(invalid="ignore"):
+        h_err = np.abs(g["h_target"] - ref["h_target"]) / (np.abs(ref["h_target"]) + 1e-12)
+        p_err = np.abs(g["p_target_y"] - ref["p_target_y"]) / (np.abs(ref["p_target_y"]) + 1e-300)
+    fin = has & np.isfinite(ref["h_target"]) & np.isfinite(h_err)
+    if fin.any():
+        rep.max_h_err = float(h_err[fin].max())
+        rep.max_p_rel_err = float(p_err[fin & np.isfinite(p_err)].max())
+    # decisions
+    gk, ga = g["key_mask"].astype(bool), g["accepted"].astype(bool)
+    rk, ra = ref["key"].astype(bool), ref["accepted"].astype(bool)
+    for b in np.nonzero(ok_seq)[0]:
+        n = int(ev[b])
+        div = None
+        for j in range(n):
+            if gk[b, j] != rk[b, j]:
+                div = ("key", j, ref["margin_key"][b, j] < EPS_LAMBDA)
+                break
+            if ga[b, j] != ra[b, j]:
+                div = ("accepted", j, ref["margin_u"][b, j] < EPS_U)
+                break
+        if div is None:
+            same = (int(g["accepted_count"][b]) == int(ref["k"][b])
+                    and int(g["extra_source"][b]) == int(ref["extra_source"][b])
+                    and int(g["key_count"][b]) == int(ref["key_count"][b]))
+            if not same:
+                rep.mismatches.append((int(b), "round", int(g["accepted_count"][b]),
+                                       int(ref["k"][b])))
+            elif int(g["extra_token"][b]) != int(ref["extra_token"][b]):
+                if ref["margin_extra"][b] < EPS_CDF:
+                    rep.eps_events += 1
+                else:
+                    rep.mismatches.append((int(b), "extra_token", int(g["extra_token"][b]),
+                                           int(ref["extra_token"][b]),
+                                           float(ref["margin_extra"][b])))
+        else:
+            what, j, excused = div
+            if excused:
+                rep.eps_events += 1
+            else:
+                rep.mismatches.append((int(b), j, "decision:" + what))
+    return rep
+
+
+def gpu_window(verifier, draft, target, tokens, V: int, tau: float, crit, seed: int,
+               window: int = 0, out=None, raise_on_status: bool = True):
+    """One dsdv_verify launch with per-position outputs; host dict of results."""
+    from paper_2511_11733_b200.dsdv import VerifyParams
+    p = VerifyParams(gamma=tokens.shape[1], tau=tau, ratio_limit=crit.ratio_limit,
+                     gap_limit=crit.gap_limit, overlap_floor=crit.overlap_floor,
+                     top_m=crit.top_m, seed=seed, window=window)
+    o = verifier.verify(draft, target, tokens, p, vocab=V, out=out)
+    if raise_on_status:
+        verifier.sync(p, o, batch=tokens.shape[0], vocab=V)
+    else:
+        torch.cuda.synchronize()
+    return o.to_host()
+
+
+def host_logits(t: torch.Tensor) -> np.ndarray:
+    """Host copy for Oracle.verify_batch: fp32 as is, bf16 as raw bits."""
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.float().cpu().numpy()
+
+
 def run_gpu_window(verifier, dtype: torch.dtype, B: int, G: int, V: int, tau: float, crit,
                    seed: int = 1, window: int = 0, logits_seed: int = 42, stride=None,
                    oracle: Oracle | None = None):

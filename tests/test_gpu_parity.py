@@ -126,11 +126,22 @@ def test_draft_sample_matches_oracle(verifier, oracle):
     B, G, V = 16, 4, 32000
     draft, _ = verifier.synth_logits(B, G, V, torch.float32, logits_seed=13)
     p = VerifyParams(gamma=G, seed=21, window=3)
-    tok = verifier.draft_sample(draft, p, vocab=V)
+    tok = verifier.draft_sample(draft, p, vocab=V).cpu().numpy()
     torch.cuda.synchronize()
-    ref = oracle_draft_tokens(oracle, host_rows(draft, V), 21, 3)
-    mism = (tok.cpu().numpy() != ref).sum()
-    assert mism <= 1, mism
+    from oracle.oracle_lib import window_uniforms
+    from tests.parity_util import EPS_CDF
+    rows = host_rows(draft, V)
+    U = window_uniforms(21, 3, B, G)
+    eps = 0
+    for b in range(B):
+        st, ref, margins = oracle.draft_tokens(rows[b], U[b, :G])
+        assert st == 0
+        for j in range(G):
+            if tok[b, j] != ref[j]:
+                # only a draw within eps of a CDF boundary may land on the neighbour
+                assert margins[j] < EPS_CDF, (b, j, tok[b, j], ref[j], margins[j])
+                eps += 1
+    assert eps <= 2, eps
 
 
 @pytest.mark.parametrize("T", [0.0, 0.5, 1.7])
@@ -144,12 +155,19 @@ def test_draft_sample_under_temperature(verifier, ref_oracle, T):
     draft, _ = verifier.synth_logits(B, G, V, torch.float32, logits_seed=17)
     p = VerifyParams(gamma=G, seed=5, window=2)
     tok = verifier.draft_sample(draft, p, vocab=V, temperature=T).cpu().numpy()
+    from oracle.oracle_lib import Oracle
+    from tests.parity_util import EPS_CDF
     rows = host_rows(draft, V)
     U = window_uniforms(5, 2, B, G)
-    mism = 0
+    port = Oracle()
+    eps = 0
     for b in range(B):
         for j in range(G):
             _, pr = ref_oracle.softmax(rows[b, j])
             q = ref_oracle.temperature_scale(pr, T)
-            mism += int(ref_oracle.sample_with_uniform(q, U[b, j])[1] != tok[b, j])
-    assert mism <= 1, mism
+            ref = ref_oracle.sample_with_uniform(q, U[b, j])[1]
+            if ref != tok[b, j]:
+                _, margin = port.sample_with_margin(q, U[b, j])
+                assert margin < EPS_CDF, (b, j, tok[b, j], ref, margin)
+                eps += 1
+    assert eps <= 2, eps

@@ -212,3 +212,77 @@ def test_errors_follow_the_reference_taxonomy(oracle):
     tl2[0, :] = -np.inf
     r = oracle.verify_window(dl, tl2, [0, 0], 0.2, c, U)
     assert r["status"] == E_INVARIANT
+
+
+# ---------------------------------------------------------------- batched checker
+@pytest.mark.parametrize("as_bf16", [False, True])
+def test_verify_batch_matches_per_window_oracle(oracle, as_bf16):
+    """Oracle.verify_batch (the checker of the full-window GPU tests) equals the
+    per-sequence restatement on every field, for several configurations that
+    share the softmaxed rows, with strided rows and bf16 bit inputs."""
+    import torch
+    from tests.parity_util import compare_batch, position_stats
+    rng = np.random.default_rng(21 + as_bf16)
+    B, G, V, stride = 7, 4, 1500, 1504
+    d = np.zeros((B, G, stride), np.float32)
+    t = np.zeros((B, G + 1, stride), np.float32)
+    for b in range(B):
+        dl, tl = _random_window(rng, G, V, scale=2.0 + b)
+        d[b, :, :V], t[b, :, :V] = dl, tl
+    if as_bf16:
+        d = torch.from_numpy(d).bfloat16().float().numpy()
+        t = torch.from_numpy(t).bfloat16().float().numpy()
+    U = window_uniforms(5, 3, B, G)
+    tok = np.zeros((B, G), np.int32)
+    for b in range(B):
+        tok[b] = oracle.draft_tokens(d[b, :, :V].astype(np.float64), U[b, :G])[1]
+    tok[2, 1] = V + 3  # an out-of-vocabulary token -> InvariantError for that sequence
+    cfgs = [(0.2, oracle.crit(2.0, 0.2, 0.5, 10)), (0.0, oracle.crit(1.2, 0.05, 0.8, 4)),
+            (0.5, oracle.crit(float("inf"), 1.0, 0.0, 1))]
+    if as_bf16:
+        dd = torch.from_numpy(d).bfloat16().view(torch.int16).numpy().view(np.uint16)
+        tt = torch.from_numpy(t).bfloat16().view(torch.int16).numpy().view(np.uint16)
+    else:
+        dd, tt = d, t
+    res = oracle.verify_batch(dd, tt, tok, cfgs, U, V, all_positions=True, nthreads=3)
+    for (tau, c), r in zip(cfgs, res):
+        for b in range(B):
+            w = oracle.verify_window(d[b, :, :V].astype(np.float64),
+                                     t[b, :, :V].astype(np.float64), tok[b], tau, c, U[b])
+            assert r["k"][b] == w["accepted_count"]
+            assert r["extra_token"][b] == w["extra_token"]
+            assert r["status"][b] == w["status"]
+            assert r["evaluated"][b] == w["evaluated"]
+            n = w["evaluated"]
+            assert (r["key"][b, :n] == w["key"][:n]).all()
+            assert (r["accepted"][b, :n] == w["accepted"][:n]).all()
+            assert np.array_equal(r["accept_prob"][b, :n], w["accept_prob"][:n])
+            assert np.array_equal(r["h_target"][b, :n], w["h_target"][:n])
+            if w["status"] != 0:
+                continue
+            for j in range(n, G):
+                if not 0 <= tok[b, j] < V:
+                    assert np.isnan(r["h_target"][b, j])
+                    continue
+                ps = position_stats(oracle, d[b, j, :V].astype(np.float64),
+                                    t[b, j, :V].astype(np.float64), int(tok[b, j]), tau, c)
+                assert ps is not None
+                assert r["h_draft"][b, j] == ps["h_draft"]
+                assert r["norm_match"][b, j] == ps["norm_match"]
+                assert bool(r["key"][b, j]) == ps["key"]
+                assert r["accept_prob"][b, j] == ps["accept_prob"]
+        # the checker accepts the oracle's own answers as a "GPU" result
+        gpu = {"status": r["status"], "accepted_count": r["k"], "extra_token": r["extra_token"],
+               "extra_source": r["extra_source"], "key_count": r["key_count"],
+               "key_mask": r["key"], "accepted": r["accepted"], "accept_prob": r["accept_prob"],
+               "h_target": r["h_target"], "h_draft": r["h_draft"],
+               "p_target_y": r["p_target_y"], "p_draft_y": r["p_draft_y"],
+               "norm_match": r["norm_match"], "p_effective_y": r["p_eff_y"]}
+        rep = compare_batch(r, gpu)
+        assert rep.ok(), rep.mismatches[:5]
+        assert rep.eps_events == 0
+        # and flags a flipped decision outside the epsilon band
+        bad = {k: np.array(v, copy=True) for k, v in gpu.items()}
+        b0 = int(np.nonzero(r["status"] == 0)[0][0])
+        bad["accepted_count"][b0] += 1
+        assert not compare_batch(r, bad).ok()
