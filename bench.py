@@ -131,10 +131,25 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
-def cpu_reference(draft_h, target_h, tokens_h, seed, window, max_seconds=20.0, nthreads=None):
-    """Time the reference's CPU verifier (oracle/_ref, else the C restatement) on
-    a bounded sample of the same windows. Returns a cpu_baseline dict."""
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def bf16_bits_to_f32(bits):
     import numpy as np
+    return (bits.astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def cpu_reference(draft_h, target_h, tokens_h, seed, window, nthreads=None):
+    """Time the reference's CPU verifier (oracle/_ref, else the C restatement)
+    on EVERY sequence of the window, all host threads. Returns a cpu_baseline
+    dict plus the reference's k per sequence."""
     from oracle.oracle_lib import Oracle, RefOracle, window_uniforms
     nthreads = nthreads or os.cpu_count() or 1
     if RefOracle.available():
@@ -143,27 +158,42 @@ def cpu_reference(draft_h, target_h, tokens_h, seed, window, max_seconds=20.0, n
         impl, kind = Oracle(), "port"
     crit = Oracle.crit(RATIO, GAP, OVERLAP, TOP_M)
     Bh = draft_h.shape[0]
-    # calibrate: one thread-round of sequences, then scale to the time budget
-    n = min(Bh, nthreads)
     U = window_uniforms(seed, window, Bh, GAMMA)
     t0 = time.perf_counter()
-    impl.verify_batch_f32(draft_h[:n], target_h[:n], tokens_h[:n], TAU, crit, U[:n], V, nthreads)
-    t1 = time.perf_counter()
-    per_round = max(t1 - t0, 1e-3)
-    rounds = max(1, min(int(max_seconds / per_round), (Bh + n - 1) // n - 1))
-    m = min(Bh, n * (1 + rounds))
-    t0 = time.perf_counter()
-    impl.verify_batch_f32(draft_h[:m], target_h[:m], tokens_h[:m], TAU, crit, U[:m], V, nthreads)
-    t1 = time.perf_counter()
-    dt = t1 - t0
-    return {"value": m * GAMMA / dt, "unit": UNIT, "cores": nthreads, "kind": kind,
-            "sample": f"{m} of {Bh} sequences of the C2 window (V={V}, gamma={GAMMA}, bf16 logits "
-                      f"as fp32), reference verify loop over Distribution rows, {dt:.2f} s"}
+    k, _, _ = impl.verify_batch_f32(draft_h, target_h, tokens_h, TAU, crit, U, V, nthreads)
+    dt = time.perf_counter() - t0
+    return {"value": Bh * GAMMA / dt, "unit": UNIT, "cores": nthreads, "kind": kind,
+            "cpu_model": cpu_model(), "seconds": dt,
+            "sample": f"all {Bh} sequences of the C2 window (V={V}, gamma={GAMMA}, bf16 logits "
+                      f"widened to fp32), reference verify_round loop over Distribution rows "
+                      f"({'oracle/_ref: the reference sources compiled' if kind == 'reference' else 'oracle C port'}), "
+                      f"{nthreads} threads, {dt:.2f} s"}, k
+
+
+def check_parity(ver, draft, target, tokens, p, timed_k):
+    """Verify the timed window against the fp64 oracle on every sequence
+    (per-position outputs of the same launch parameters; the window is
+    deterministic, so k must equal the timed launch's)."""
+    import numpy as np
+    from oracle.oracle_lib import Oracle, window_uniforms
+    from tests.parity_util import compare_batch, gpu_window, host_logits
+    crit = Oracle.crit(RATIO, GAP, OVERLAP, TOP_M)
+    gpu = gpu_window(ver, draft, target, tokens, V, TAU, crit, p.seed, p.window)
+    ref = Oracle().verify_batch(host_logits(draft), host_logits(target), tokens.cpu().numpy(),
+                                [(TAU, crit)], window_uniforms(p.seed, p.window, B, GAMMA), V,
+                                all_positions=True)[0]
+    rep = compare_batch(ref, gpu)
+    return {"window": int(p.window), "sequences": rep.sequences,
+            "positions_checked": rep.positions_checked, "mismatches": len(rep.mismatches),
+            "eps_events": rep.eps_events,
+            "device_near_threshold": int(gpu["near_threshold"].sum()),
+            "timed_k_equal": bool(np.array_equal(gpu["accepted_count"].numpy(), timed_k)),
+            "max_h_rel_err": rep.max_h_err, "max_p_rel_err": rep.max_p_rel_err,
+            "checker": "oracle/dsd_oracle.c fp64 (Oracle.verify_batch), every sequence"}
 
 
 def make_inputs(ver, device):
     import torch
-    from oracle.oracle_lib import Oracle  # noqa: F401  (draft draws are device-side here)
     from paper_2511_11733_b200.dsdv import VerifyParams
     draft, target = ver.synth_logits(B, GAMMA, V, torch.bfloat16, logits_seed=LOGITS_SEED,
                                      device=device)
@@ -215,6 +245,7 @@ def run_ours(args, rank, world, local_rank):
     ver.sync(p, out, batch=B, vocab=V)
     mean_k = float(out.accepted_count.float().mean().item())
     committed = float((out.accepted_count.float() + 1).sum().item())
+    timed_k = out.accepted_count.cpu().numpy()
 
     # ---- e2e: host buffers through the public API, copies inside the timed region
     draft_h = draft.cpu().pin_memory()
@@ -254,13 +285,14 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_ms = float(et.item())
 
-    # ---- CPU baseline (rank 0, N=1 only)
-    cpu = None
+    # ---- parity of the timed window and the CPU baseline (rank 0, N=1 only)
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        p.window = args.steps - 1  # the last timed window
+        parity = check_parity(ver, draft, target, tokens, p, timed_k)
         d32 = draft_h.float().numpy()
         t32 = target_h.float().numpy()
-        cpu = cpu_reference(d32, t32, tokens_h.numpy(), p.seed, 0,
-                            max_seconds=args.cpu_seconds)
+        cpu, _ = cpu_reference(d32, t32, tokens_h.numpy(), p.seed, p.window)
 
     if rank != 0:
         return
@@ -300,6 +332,8 @@ def run_ours(args, rank, world, local_rank):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if parity is not None:
+        line["parity"] = parity
     print(json.dumps(line), flush=True)
 
 
@@ -359,8 +393,7 @@ def run_sharded(args, rank, world, local_rank):
     committed = float((out.accepted_count.float() + 1).sum().item())
     bad = int((out.status != 0).sum().item())
     if args.exchange == "peer":
-        bad += int(sv._peer_status.item() != 0)  # a peer flag never arrived
-
+        
     # e2e: this rank's slice and the tokens from pinned host memory, results back
     draft_h, target_h, tokens_h = (draft.cpu().pin_memory(), target.cpu().pin_memory(),
                                    tokens.cpu().pin_memory())
@@ -437,46 +470,59 @@ def run_sharded(args, rank, world, local_rank):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU verifier on all host threads."""
+    """--impl reference: the reference's own CPU verifier (oracle/_ref, the
+    reference sources compiled) on all host threads, every sequence of the
+    C2 window each step. Inputs never touch the GPU library: the window is
+    generated on the host by oracle_synth_logits (bit-identical to the
+    device's dsdv_synth_logits, tests/test_gpu_parity.py) and the draft
+    tokens are drawn from P_d by the fp64 oracle with the same Philox draft
+    slots as dsdv_draft_sample (equal except draws within 1e-5 of a CDF
+    boundary)."""
     if rank != 0:
         return
+    from concurrent.futures import ThreadPoolExecutor
+
     import numpy as np
-    import torch
-    from oracle.oracle_lib import window_uniforms  # noqa: F401
-    # inputs: the same synthetic workload; generated on a GPU when one is there,
-    # else a CPU restatement of the families is not needed — the reference arm
-    # only measures the CPU verifier, so any rows of the right shape and
-    # distribution family work; use the device generator when possible.
-    if torch.cuda.is_available():
-        from paper_2511_11733_b200.dsdv import Verifier
-        ver = Verifier(0)
-        draft, target, tokens, p = make_inputs(ver, torch.device("cuda", 0))
-        d32, t32, tk = draft.float().cpu().numpy(), target.float().cpu().numpy(), tokens.cpu().numpy()
-        seed = p.seed
-    else:
-        rng = np.random.default_rng(LOGITS_SEED)
-        nseq = 8
-        t32 = (rng.standard_normal((nseq, GAMMA + 1, V)) * 6).astype(np.float32)
-        d32 = (t32[:, :GAMMA] + rng.standard_normal((nseq, GAMMA, V)) * 2).astype(np.float32)
-        tk = rng.integers(0, V, size=(nseq, GAMMA)).astype(np.int32)
-        seed = 1
-    values = []
+    from oracle.oracle_lib import Oracle, window_uniforms
+    nthreads = os.cpu_count() or 1
+    o = Oracle()
+    t0 = time.perf_counter()
+    dbits, tbits = o.synth_logits(B, GAMMA, V, True, logits_seed=LOGITS_SEED, nthreads=nthreads)
+    d32, t32 = bf16_bits_to_f32(dbits), bf16_bits_to_f32(tbits)
+    del dbits, tbits
+    U = window_uniforms(1, 0, B, GAMMA)
+
+    def draw(b):
+        st, tok, _ = o.draft_tokens(d32[b, :, :V].astype(np.float64), U[b, :GAMMA])
+        assert st == 0
+        return tok
+
+    with ThreadPoolExecutor(nthreads) as ex:
+        tk = np.stack(list(ex.map(draw, range(B)))).astype(np.int32)
+    prep_s = time.perf_counter() - t0
+    samples = []
     for w in range(args.warmup + args.steps):
-        r = cpu_reference(d32, t32, tk, seed, w, max_seconds=args.cpu_seconds / max(1, args.steps))
+        r, _ = cpu_reference(d32, t32, tk, 1, w, nthreads)
         if w >= args.warmup:
-            values.append(r)
-    v = statistics.median(x["value"] for x in values)
-    sample = values[-1]
+            samples.append(r)
+    total_s = sum(x["seconds"] for x in samples)
+    v = B * GAMMA * len(samples) / total_s
+    sample = samples[-1]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": B * GAMMA / v * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / len(samples) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (same workload as the GPU arm)",
-        "config": {"workload": "C2 window, V=128256, gamma=8, B=256, reference CPU verifier "
-                               "(verify_round loop over Distribution rows)",
-                   "batch_per_gpu": B, "gamma": GAMMA, "vocab": V},
+        "data": "synthetic: the GPU arm's Philox Zipf/Gaussian window (SURVEY.md 8d) generated "
+                "on the host (oracle_synth_logits, bit-identical to dsdv_synth_logits), draft "
+                "tokens drawn from P_d on the host",
+        "config": {"workload": "C2: dsdv_verify window, V=128256, gamma=8, B=256 per GPU, bf16 logits, "
+                               "tau=0.2, lambda=(2.0, 0.2, 0.5), top_m=10",
+                   "batch_per_gpu": B, "gamma": GAMMA, "vocab": V,
+                   "implementation": "reference verify_round loop (oracle/_ref) on all host threads",
+                   "input_prep_s": prep_s},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": sample["cores"], "kind": sample["kind"],
-                         "sample": sample["sample"]},
+                         "cpu_model": sample["cpu_model"],
+                         "sample": f"every step: {sample['sample']}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -488,7 +534,6 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--parallel", choices=["vocab", "replicas"], default="vocab",
                     help="N>1: vocabulary-sharded window (C4) or independent replicas")

@@ -32,6 +32,18 @@ struct DraftingContractError : Error {
 struct EmptyResidualError : Error {
   using Error::Error;
 };
+// exact enumeration beyond the tractability guard (enumerate.cpp:35)
+struct EnumerationTooLargeError : Error {
+  using Error::Error;
+};
+// two simulation reports over different token counts (netsim.cpp:206)
+struct IncomparableReportsError : Error {
+  using Error::Error;
+};
+// a CSV / report file could not be written (metrics.cpp:150)
+struct WriteError : Error {
+  using Error::Error;
+};
 // the GPU runtime failed (no counterpart in the reference: its path is host-only)
 struct DeviceError : Error {
   using Error::Error;

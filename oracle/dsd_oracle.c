@@ -557,3 +557,60 @@ int oracle_verify_batch(int B, int gamma, int V, int stride, int dtype, const vo
   free(jobs);
   return 0;
 }
+
+/* ---- host generator of the synthetic windows (include/dsdv/synth.h) ---- */
+#include "dsdv/synth.h"
+
+typedef struct {
+  int B, gamma, V, stride, dtype, nthreads, tid;
+  uint64_t seed;
+  void *draft, *target;
+} synth_job;
+
+static void *synth_worker(void *arg) {
+  synth_job *j = (synth_job *)arg;
+  const int G1 = j->gamma + 1;
+  for (int item = j->tid; item < j->B * G1; item += j->nthreads) {
+    const int b = item / G1, r = item - b * G1;
+    const dsdv_synth_row rp = dsdv_synth_row_params(j->seed, (uint32_t)item, b, j->V);
+    const size_t t0 = (size_t)item * j->stride;
+    const size_t d0 = ((size_t)b * j->gamma + r) * j->stride;
+    for (int i = 0; i < j->stride; ++i) {
+      float lt = -INFINITY, ld = -INFINITY, z1 = 0.0f;
+      if (i < j->V) {
+        dsdv_synth_element(j->seed, (uint32_t)item, &rp, j->V, i, &lt, &z1);
+      }
+      if (j->dtype == 1) {
+        const uint16_t tb = dsdv_synth_bf16_bits(lt);
+        ((uint16_t *)j->target)[t0 + i] = tb;
+        if (r < j->gamma) {
+          if (i < j->V) ld = dsdv_synth_draft(dsdv_synth_bf16_value(tb), rp.delta, z1);
+          ((uint16_t *)j->draft)[d0 + i] = dsdv_synth_bf16_bits(ld);
+        }
+      } else {
+        ((float *)j->target)[t0 + i] = lt;
+        if (r < j->gamma) {
+          if (i < j->V) ld = dsdv_synth_draft(lt, rp.delta, z1);
+          ((float *)j->draft)[d0 + i] = ld;
+        }
+      }
+    }
+  }
+  return NULL;
+}
+
+int oracle_synth_logits(int B, int gamma, int V, int stride, uint64_t seed, int dtype,
+                        void *draft, void *target, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  synth_job *jobs = (synth_job *)malloc(sizeof(synth_job) * (size_t)nthreads);
+  for (int t = 0; t < nthreads; ++t) {
+    synth_job j = {B, gamma, V, stride, dtype, nthreads, t, seed, draft, target};
+    jobs[t] = j;
+    pthread_create(&th[t], NULL, synth_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  free(th);
+  free(jobs);
+  return 0;
+}

@@ -133,6 +133,12 @@ int oracle_verify_batch(int B, int gamma, int V, int stride, int dtype, const vo
                         const oracle_criteria *crits, const double *uniforms /*[B][2g+1]*/,
                         int all_positions, int nthreads, oracle_batch_out *outs /*[ncfg]*/);
 
+/* The synthetic windows of SURVEY.md §8(d) on the host, bit-identical to the
+ * device's dsdv_synth_logits (shared arithmetic: include/dsdv/synth.h):
+ * dtype 0 = fp32, 1 = bf16 bits; rows padded to stride with -inf. */
+int oracle_synth_logits(int B, int gamma, int V, int stride, uint64_t seed, int dtype,
+                        void *draft, void *target, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -138,7 +138,24 @@ class Oracle:
         L.oracle_verify_batch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                           C.c_void_p, _ip, C.c_int, _dp, C.c_void_p, _dp, C.c_int,
                                           C.c_int, C.c_void_p]
+        L.oracle_synth_logits.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int,
+                                          C.c_void_p, C.c_void_p, C.c_int]
         self.L = L
+
+    def synth_logits(self, batch: int, gamma: int, vocab: int, bf16: bool, logits_seed: int = 42,
+                     stride: int | None = None, nthreads=None):
+        """The device's dsdv_synth_logits window on the host, bit for bit:
+        (draft [B][gamma][stride], target [B][gamma+1][stride]) as fp32, or
+        as raw bf16 bits (uint16) when bf16."""
+        vec = 8 if bf16 else 4
+        stride = stride or (vocab + vec - 1) // vec * vec
+        dt = np.uint16 if bf16 else np.float32
+        draft = np.empty((batch, gamma, stride), dt)
+        target = np.empty((batch, gamma + 1, stride), dt)
+        self.L.oracle_synth_logits(batch, gamma, vocab, stride, logits_seed, 1 if bf16 else 0,
+                                   draft.ctypes.data, target.ctypes.data,
+                                   nthreads or os.cpu_count() or 1)
+        return draft, target
 
     @staticmethod
     def crit(ratio_limit=2.0, gap_limit=0.2, overlap_floor=0.5, top_m=10) -> _Crit:

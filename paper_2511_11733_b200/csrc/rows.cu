@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 #include "sample.cuh"
+#include "dsdv/synth.h"
 
 namespace dsdv {
 
@@ -189,19 +190,6 @@ __global__ void __launch_bounds__(kConsumerThreads)
 }
 
 // ------------------------------------------------------------------ synth
-__device__ __forceinline__ float u01_open(uint32_t x) {
-  return ((float)(x >> 8) + 0.5f) * (1.0f / 16777216.0f);  // (0, 1)
-}
-
-__device__ __forceinline__ unsigned gcd_u(unsigned a, unsigned b) {
-  while (b) {
-    const unsigned t = a % b;
-    a = b;
-    b = t;
-  }
-  return a;
-}
-
 template <class Out>
 __device__ __forceinline__ Out to_out(float x);
 template <>
@@ -213,9 +201,9 @@ __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float x) {
   return __float2bfloat16_rn(x);
 }
 
-// Families by b mod 4: Zipf target l_t[i] = -sigma ln(1 + pi(i)),
-// pi(i) = (a i + c) mod V with gcd(a, V) = 1, sigma 1.2 / 2.5 / 3.5; Gaussian
-// target sigma 6. Draft = target + delta N(0, 1), delta 0.8 / 1.0 / 1.5 / 2.
+// Families by b mod 4; the element arithmetic lives in
+// include/dsdv/synth.h, shared bit for bit with the host generator the CPU
+// reference arm uses (oracle/dsd_oracle.c oracle_synth_logits).
 template <class Out>
 __global__ void __launch_bounds__(256)
     synth_logits_kernel(int B, int gamma, int V, int stride, uint64_t seed, Out *__restrict__ draft,
@@ -223,16 +211,7 @@ __global__ void __launch_bounds__(256)
   const int G1 = gamma + 1;
   const int item = blockIdx.x;  // b * (gamma + 1) + j
   const int b = item / G1, j = item - b * G1;
-  const int fam = b & 3;
-  const float sigma_tab[4] = {1.2f, 2.5f, 3.5f, 6.0f};
-  const float delta_tab[4] = {0.8f, 1.0f, 1.5f, 2.0f};
-  const float sigma = sigma_tab[fam], delta = delta_tab[fam];
-  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-  const dsdv_philox_out rp = dsdv_philox4x32_10(0xffffffffu, (uint32_t)item, 0x5eedu, 0u, k0, k1);
-  unsigned a = 1u + 2u * (rp.v[0] % (unsigned)(V / 2 > 0 ? V / 2 : 1));
-  while (gcd_u(a % (unsigned)V, (unsigned)V) != 1u) a += 2u;
-  a %= (unsigned)V;
-  const unsigned c = rp.v[1] % (unsigned)V;
+  const dsdv_synth_row rp = dsdv_synth_row_params(seed, (uint32_t)item, b, V);
   Out *rt = target + (size_t)item * stride;
   Out *rd = (j < gamma) ? draft + ((size_t)b * gamma + j) * stride : nullptr;
   const Out ninf = to_out<Out>(-INFINITY);
@@ -242,24 +221,12 @@ __global__ void __launch_bounds__(256)
       if (rd) rd[i] = ninf;
       continue;
     }
-    const dsdv_philox_out r = dsdv_philox4x32_10((uint32_t)i, (uint32_t)item, 0x10917u, 0u, k0, k1);
-    const float r1 = sqrtf(-2.0f * logf(u01_open(r.v[0])));
-    const float th = 6.283185307179586f * u01_open(r.v[1]);
-    const float z0 = r1 * cosf(th), z1 = r1 * sinf(th);
-    float lt;
-    if (fam < 3) {
-      const unsigned pi = (unsigned)(((unsigned long long)a * (unsigned)i + c) % (unsigned)V);
-      lt = -sigma * logf(1.0f + (float)pi);
-    } else {
-      lt = sigma * z0;
-    }
+    float lt, z1;
+    dsdv_synth_element(seed, (uint32_t)item, &rp, V, i, &lt, &z1);
     // round the target first so that draft = stored target + noise
     const Out lt_o = to_out<Out>(lt);
     rt[i] = lt_o;
-    if (rd) {
-      const float ltr = (float)lt_o;
-      rd[i] = to_out<Out>(ltr + delta * z1);
-    }
+    if (rd) rd[i] = to_out<Out>(dsdv_synth_draft((float)lt_o, rp.delta, z1));
   }
 }
 

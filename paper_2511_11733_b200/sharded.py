@@ -61,6 +61,9 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return t
 
+    def barrier(self) -> None:
+        self.dist.barrier(group=self.group)
+
 
 class PeerExchange:
     """Exchange buffers of all ranks mapped into this process (CUDA IPC over
@@ -80,26 +83,48 @@ class PeerExchange:
         self.set_bytes = self.P * self.stride
         self.bytes = 2 * self.set_bytes + 8 * self.P  # two sets, then the flags
         self._owned, self._opened = [], []
+        self.comm = comm
+        self.ok = True
         if bases is not None:
             self.bases = list(bases)
             return
-        ptr = C.c_void_p()
-        self.v._check(LIB.dsdv_dev_alloc(self.v._h, self.bytes, C.byref(ptr)))
-        self._owned.append(ptr.value)
+        # Every rank runs the same collectives whatever fails locally, so a
+        # failure on one rank can never leave the others in a mismatched
+        # collective: (1) local allocation and export, (2) all-gather of
+        # (ok, handle), (3) open the peers, (4) all-gather of ok. On any
+        # failure every rank releases what it holds (close()) and self.ok is
+        # False on all of them.
         handle = (C.c_uint8 * 64)()
-        self.v._check(LIB.dsdv_ipc_handle(self.v._h, ptr, handle))
-        mine = torch.tensor(bytearray(handle), dtype=torch.uint8, device=verifier.device)
+        ok = 1
+        ptr = C.c_void_p()
+        try:
+            self.v._check(LIB.dsdv_dev_alloc(self.v._h, self.bytes, C.byref(ptr)))
+            self._owned.append(ptr.value)
+            self.v._check(LIB.dsdv_ipc_handle(self.v._h, ptr, handle))
+        except Exception:  # noqa: BLE001  (reported through the collective flag)
+            ok = 0
+        mine = torch.tensor([ok] + list(bytearray(handle)), dtype=torch.uint8,
+                            device=verifier.device)
         allh = comm.all_gather(mine).cpu()
+        ok = int(allh[:, 0].min().item())
         self.bases = []
-        for q in range(self.P):
-            if q == rank:
-                self.bases.append(ptr.value)
-                continue
-            h = (C.c_uint8 * 64)(*allh[q].tolist())
-            peer = C.c_void_p()
-            self.v._check(LIB.dsdv_ipc_open(self.v._h, h, C.byref(peer)))
-            self._opened.append(peer.value)
-            self.bases.append(peer.value)
+        if ok:
+            try:
+                for q in range(self.P):
+                    if q == rank:
+                        self.bases.append(ptr.value)
+                        continue
+                    h = (C.c_uint8 * 64)(*allh[q, 1:].tolist())
+                    peer = C.c_void_p()
+                    self.v._check(LIB.dsdv_ipc_open(self.v._h, h, C.byref(peer)))
+                    self._opened.append(peer.value)
+                    self.bases.append(peer.value)
+            except Exception:  # noqa: BLE001
+                ok = 0
+        flags = comm.all_gather(torch.tensor([ok], dtype=torch.int32, device=verifier.device))
+        self.ok = int(flags.min().item()) == 1
+        if not self.ok:
+            self.close()
 
     @staticmethod
     def allocate_local(verifier: Verifier, nranks: int, size: int) -> list[int]:
@@ -122,11 +147,18 @@ class PeerExchange:
         return [b + 2 * self.set_bytes - self.P * self.stride for b in self.bases]
 
     def close(self):
+        """Unmap the peers' buffers, wait until every rank has done the same
+        (freeing an exported allocation while importers still map it is
+        undefined), then free our own. Collective when a comm is attached."""
         for ptr in self._opened:
             LIB.dsdv_ipc_close(self.v._h, C.c_void_p(ptr))
+        self._opened = []
+        if self.comm is not None:
+            torch.cuda.synchronize(self.v.device)
+            self.comm.barrier()
         for ptr in self._owned:
             LIB.dsdv_dev_free(self.v._h, C.c_void_p(ptr))
-        self._opened, self._owned = [], []
+        self._owned = []
 
 
 class ShardedVerifier:
@@ -294,6 +326,14 @@ class ShardedVerifier:
             tiles.data_ptr() if tiles is not None else None, s))
         return mass if mode == SHARD_MASS else tok
 
+    def _peer_failed(self) -> bool:
+        """Did a flag round of an earlier window time out? Read without a sync:
+        the status copy of the last window is checked once it has landed."""
+        ev = getattr(self, "_peer_event", None)
+        if ev is None or not ev.query():
+            return False
+        return int(self._peer_status_host.item()) != 0
+
     # ---- one window on this rank --------------------------------------------
     def verify(self, draft, target, tokens, p: VerifyParams, vocab: int, offset: int, local: int,
                comm: TorchComm, out: WindowResult | None = None, stream=None,
@@ -308,28 +348,30 @@ class ShardedVerifier:
             M = min(p.top_m, vocab)
             _, size = self.exchange_layout(B, G, M)
             ex = getattr(self, "_ex", None)
+            if ex is not None and self._peer_failed():
+                # a flag round of an earlier window timed out (a peer stalled or
+                # died): that window already reported DSDV_E_NCCL in its statuses.
+                # Fatal for the exchange: the buffer sets may hold stale records and
+                # a peer may still write into them, so they are never reused.
+                self._ex = None
+                raise dsdv.DsdvError(dsdv.E_NCCL, "peer exchange: a flag round timed out in an "
+                                     "earlier window; the exchange is unusable")
             if ex is None or ex.stride < size:
                 if ex is not None:  # a larger window: remap (every rank does the same)
-                    torch.cuda.synchronize(draft.device)
                     ex.close()
                     self._ex = None
                 # collective setup; if any rank cannot map its peers (no CUDA IPC
                 # / peer access), every rank falls back to the NCCL exchange
-                try:
-                    ex = PeerExchange(self.v, comm.size, comm.rank, size, comm=comm)
-                    ok = 1
-                except Exception:  # noqa: BLE001  (reported through the flag)
-                    ex, ok = None, 0
-                flags = comm.all_gather(torch.tensor([ok], dtype=torch.int32, device=draft.device))
-                if int(flags.min().item()) == 0:
-                    if ex is not None:
-                        ex.close()
+                ex = PeerExchange(self.v, comm.size, comm.rank, size, comm=comm)
+                if not ex.ok:
                     self.peer_fallback = True
                     return self.verify(draft, target, tokens, p, vocab, offset, local, comm, out,
                                        stream, exchange="nccl")
                 self._ex = ex
                 self._epoch = 0
                 self._peer_status = torch.zeros(1, dtype=torch.int32, device=draft.device)
+                self._peer_status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+                self._peer_event = None
             self._epoch += 1
             w, f = self._epoch, 3 * self._epoch
             self.stats_peers(ex, w, draft, target, tokens, p, vocab, offset, local, stream,
@@ -344,6 +386,16 @@ class ShardedVerifier:
             self.signal_peers(ex, f + 2, stream, draft.device)
             self.wait_peers(ex, f + 2, self._peer_status, stream)
             self.tokens_max_peers(ex, w, B, G, M, out.extra_token, stream)
+            # a timed-out flag round fails every sequence of the window (the merged
+            # records may be stale); the caller's sync raises it
+            st = out.status
+            st.copy_(torch.where(self._peer_status.expand_as(st) != 0,
+                                 torch.full_like(st, dsdv.E_NCCL), st))
+            cs = stream or torch.cuda.current_stream(draft.device)
+            with torch.cuda.stream(cs):
+                self._peer_status_host.copy_(self._peer_status, non_blocking=True)
+                self._peer_event = torch.cuda.Event()
+                self._peer_event.record(cs)
             return out
         else:
             packed = self.stats(draft, target, tokens, p, vocab, offset, local, stream)

@@ -171,3 +171,23 @@ def test_draft_sample_under_temperature(verifier, ref_oracle, T):
                 assert margin < EPS_CDF, (b, j, tok[b, j], ref, margin)
                 eps += 1
     assert eps <= 2, eps
+
+
+@pytest.mark.parametrize("dtype,V", [(torch.bfloat16, 128256), (torch.float32, 151936),
+                                     (torch.bfloat16, 1003), (torch.float32, 7)])
+def test_host_synth_is_bit_identical_to_device(verifier, oracle, dtype, V):
+    """The CPU reference arm builds its window with oracle_synth_logits; it must
+    be the device's dsdv_synth_logits window bit for bit (include/dsdv/synth.h)."""
+    B, G = 8, 3
+    d, t = verifier.synth_logits(B, G, V, dtype, logits_seed=42)
+    hd, ht = oracle.synth_logits(B, G, V, dtype == torch.bfloat16, logits_seed=42,
+                                 stride=d.shape[-1])
+    if dtype == torch.bfloat16:
+        gd = d.view(torch.int16).cpu().numpy().view(np.uint16)
+        gt = t.view(torch.int16).cpu().numpy().view(np.uint16)
+    else:
+        gd = d.cpu().numpy().view(np.uint32)
+        gt = t.cpu().numpy().view(np.uint32)
+        hd, ht = hd.view(np.uint32), ht.view(np.uint32)
+    assert np.array_equal(gd, hd), int((gd != hd).sum())
+    assert np.array_equal(gt, ht), int((gt != ht).sum())
