@@ -77,6 +77,28 @@ def build_dsdv(force: bool = False, trace: bool = False) -> Path:
     return lib
 
 
+def build_variant(name: str, defines: list[str], force: bool = False) -> Path:
+    """libdsdv_<name>.so with extra -D flags (development aid: kernel variants
+    timed side by side on one box through DSDV_LIB)."""
+    hdrs = _headers()
+    lib = PKG / f"libdsdv_{name}.so"
+    bdir = BUILD / f"var_{name}"
+    if not force and not _stale(lib, [*(CSRC / s for s in CU_SOURCES), *hdrs]):
+        return lib
+    bdir.mkdir(parents=True, exist_ok=True)
+    flags = [*NVCC_FLAGS, *(f"-D{d}" for d in defines)]
+    objs, jobs = [], []
+    for src in CU_SOURCES:
+        s = CSRC / src
+        o = bdir / (s.stem + ".o")
+        objs.append(o)
+        jobs.append([NVCC, *flags, "-c", str(s), "-o", str(o)])
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        list(ex.map(_run, jobs))
+    _run([NVCC, *ARCH, "-shared", "-o", str(lib), *map(str, objs)])
+    return lib
+
+
 def build_dsd_api(force: bool = False) -> Path | None:
     srcs = [HOSTSRC / s for s in HOST_SOURCES if (HOSTSRC / s).exists()]
     if not srcs:
@@ -112,7 +134,10 @@ def build_all(force: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    if "--trace" in sys.argv:
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:], force=True))
+    elif "--trace" in sys.argv:
         print(build_dsdv(force="--force" in sys.argv, trace=True))
     else:
         build_all(force="--force" in sys.argv)

@@ -265,16 +265,29 @@ __device__ __forceinline__ void vstore(int *p, int v) { *(volatile int *)p = v; 
 // exponent is one FFMA: x = v * L - mtL. The epilogue converts back exactly
 // (lse_from_sum): ln sum 2^(v L) = (mtL + log2 s) ln 2, and the (1.3e-8)
 // relative error of L is corrected to first order with the row maximum.
+// fp32 sums are carried as packed f32x2 pairs (pst / psd / psz: one FADD2 per
+// two exponentials, no per-chunk horizontal adds) and folded into st / sd / sz
+// only at the end of an item (flush).
 template <class Acc>
 struct ItemState {
   Acc mt, st, md, sd, sz;  // natural-log maxima (lazy, within kSlack) and sums
   Acc mtL, mdL;            // log2 reference points of the sums
   uint32_t diff;
+  f32x2 pst, psd, psz;     // packed fp32 sums (Acc = float only)
   __device__ __forceinline__ void reset() {
     mt = md = Acc(kFloorM);
     mtL = mdL = Acc(kFloorM) * log2e<Acc>();
     st = sd = sz = Acc(0);
+    pst = psd = psz = 0ull;
     diff = 0;
+  }
+  __device__ __forceinline__ void flush() {
+    if constexpr (sizeof(Acc) == 4) {
+      st += lo2(pst) + hi2(pst);
+      sd += lo2(psd) + hi2(psd);
+      sz += lo2(psz) + hi2(psz);
+      pst = psd = psz = 0ull;
+    }
   }
 };
 
@@ -345,12 +358,12 @@ __device__ __forceinline__ Acc key_floor(int th) {
 // reach it. Only lanes whose maximum reaches the bound enter the capture, and
 // each captured element is re-read from the resident stage by its index, so
 // the divergent part costs a few instructions per captured element.
-template <class In, bool TAIL, class Acc, int VEC>
+template <class In, bool TAIL, class Acc>
 __device__ __forceinline__ void capture_row(Slot<Acc> &sl, int r, int lkey, int th,
-                                            const Acc (&v)[kVecs][VEC], const uint8_t *srow,
-                                            int c, int tid, int lane, const DevParams &p,
-                                            unsigned long long *trl) {
+                                            const uint8_t *srow, int c, int tid, int lane,
+                                            const DevParams &p, unsigned long long *trl) {
   constexpr int CH = kRowBytes / (int)sizeof(In);
+  constexpr int VEC = InTraits<In>::kVec;
   TR_INC(trl, kTrCapCalls);
   int *bins = sl.klist[r];
   const int bin = vload(bins + lane);
@@ -367,6 +380,10 @@ __device__ __forceinline__ void capture_row(Slot<Acc> &sl, int r, int lkey, int 
   if (lkey >= th) {
     const Acc thv = key_floor<Acc>(th);
     unsigned keep = 0;
+    Acc v[kVecs][VEC];  // this lane's elements, re-read from the resident stage
+#pragma unroll
+    for (int h = 0; h < kVecs; ++h)
+      unpack(lds128(srow + vec_index(h, tid >> 5, lane) * 16), v[h], (In *)nullptr);
 #pragma unroll
     for (int h = 0; h < kVecs; ++h)
 #pragma unroll
@@ -447,12 +464,48 @@ __device__ __forceinline__ void exp_sums(const double (&vt)[VEC], const double (
   }
 }
 
+// packed fp32 exponential sums of one 16-byte vector pair into the item's
+// accumulators (the reference points are not changed here)
+template <bool PAIR, bool NEEDZ, int VEC>
+__device__ __forceinline__ void exp_acc(const float (&vt)[VEC], const float (&vd)[VEC],
+                                        ItemState<float> &S, const DevParams &p) {
+  const f32x2 L2 = pk2(kLog2eF, kLog2eF);
+  const f32x2 nmt2 = pk2(-S.mtL, -S.mtL), nmd2 = pk2(-S.mdL, -S.mdL);
+  const f32x2 omt2 = pk2(p.omt_f, p.omt_f), tau2 = pk2(p.tau_f, p.tau_f);
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    const f32x2 xt = fma2(pk2(vt[e], vt[e + 1]), L2, nmt2);
+    S.pst = add2(S.pst, pk2(fast_exp2(lo2(xt)), fast_exp2(hi2(xt))));
+    if (PAIR) {
+      const f32x2 xd = fma2(pk2(vd[e], vd[e + 1]), L2, nmd2);
+      S.psd = add2(S.psd, pk2(fast_exp2(lo2(xd)), fast_exp2(hi2(xd))));
+      if (NEEDZ) {
+        const f32x2 xz = fma2(omt2, xt, mul2(tau2, xd));
+        if (e / 2 < kZMufu)
+          S.psz = add2(S.psz, pk2(fast_exp2(lo2(xz)), fast_exp2(hi2(xz))));
+        else
+          S.psz = add2(S.psz, poly_exp2x2(xz));
+      }
+    }
+  }
+}
+
+// A chunk value above the reference by more than kGuard (natural-log units)
+// could overflow the fp32 sums of a chunk folded against the old reference:
+// 2^(kGuard * log2 e + log2 8192) stays below 2^128.
+constexpr float kGuard = 60.0f;
+
 // Fold this thread's kVecs 16-byte vectors per row of one ring stage (ids of
-// vector h: c*CH + (h*kCT + tid)*VEC + e). Top-m bookkeeping is one warp max
-// per chunk and row (REDUX) — the key of block (chunk, warp) — compared with
-// the row's running bound; the rare blocks that reach it are captured
-// (capture_row). Otherwise the only control flow is the warp vote of the
-// (rare) lazy rescale.
+// vector h: c*CH + (h*kCT + tid)*VEC + e).
+//
+// fp32 accumulation (bf16 / fp32 rows): the exponentials go first, against the
+// lane's current reference points, so the MUFU work of a chunk starts as soon
+// as its vectors are unpacked; the chunk maximum, the block-maximum key
+// (REDUX) of the top-m bookkeeping, the (rare) capture and the lazy
+// reference update follow from the same registers. Only an item's first
+// chunk takes its maximum first (no reference yet). A chunk that overshoots
+// the reference by more than kGuard is folded again against the new one.
+// fp64 rows keep the max-first order.
 template <class In, bool PAIR, bool NEEDZ, bool TAIL>
 __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t *starget, int tid,
                                            int c, ItemState<typename InTraits<In>::Acc> &S,
@@ -467,47 +520,88 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
 
   Acc vt[kVecs][VEC], vd[kVecs][VEC];
   uint32_t diff = 0;
-#pragma unroll
-  for (int h = 0; h < kVecs; ++h) {
-    const int q = vec_index(h, warp, lane);
-    const uint4 a = lds128(starget + q * 16);
-    unpack(a, vt[h], (In *)nullptr);
-    if (PAIR) {
-      const uint4 bb = lds128(sdraft + q * 16);
-      unpack(bb, vd[h], (In *)nullptr);
-      diff |= (a.x ^ bb.x) | (a.y ^ bb.y) | (a.z ^ bb.z) | (a.w ^ bb.w);
-    } else {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) vd[h][e] = Acc(0);
-    }
-  }
-  if (TAIL) {
-    // elements past the logical row are -inf in both rows (no mass, equal,
-    // ranked after every real id); the equality flag sees real ids only
-    diff = 0;
+  auto load = [&]() {
 #pragma unroll
     for (int h = 0; h < kVecs; ++h) {
-      const int id0 = c * CH + vec_index(h, warp, lane) * VEC;
+      const int q = vec_index(h, warp, lane);
+      const uint4 a = lds128(starget + q * 16);
+      unpack(a, vt[h], (In *)nullptr);
+      if (PAIR) {
+        const uint4 bb = lds128(sdraft + q * 16);
+        unpack(bb, vd[h], (In *)nullptr);
+        diff |= (a.x ^ bb.x) | (a.y ^ bb.y) | (a.z ^ bb.z) | (a.w ^ bb.w);
+      } else {
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        if (id0 + e >= p.vocab_local) {
-          vt[h][e] = ni;
-          if (PAIR) vd[h][e] = ni;
-        } else if (PAIR) {
-          diff |= bits_differ(vt[h][e], vd[h][e]) ? 1u : 0u;
+        for (int e = 0; e < VEC; ++e) vd[h][e] = Acc(0);
+      }
+    }
+    if (TAIL) {
+      // elements past the logical row are -inf in both rows (no mass, equal,
+      // ranked after every real id); the equality flag sees real ids only
+      diff = 0;
+#pragma unroll
+      for (int h = 0; h < kVecs; ++h) {
+        const int id0 = c * CH + vec_index(h, warp, lane) * VEC;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          if (id0 + e >= p.vocab_local) {
+            vt[h][e] = ni;
+            if (PAIR) vd[h][e] = ni;
+          } else if (PAIR) {
+            diff |= bits_differ(vt[h][e], vd[h][e]) ? 1u : 0u;
+          }
         }
       }
     }
-  }
-  Acc cmt = ni, cmd = ni;
+  };
+  auto chunk_max = [&](Acc &cmt, Acc &cmd) {
+    cmt = ni;
+    cmd = ni;
 #pragma unroll
-  for (int h = 0; h < kVecs; ++h)
+    for (int h = 0; h < kVecs; ++h)
 #pragma unroll
-    for (int e = 0; e < VEC; e += 2) {
-      cmt = vmax3(cmt, vt[h][e], vt[h][e + 1]);
-      if (PAIR) cmd = vmax3(cmd, vd[h][e], vd[h][e + 1]);
+      for (int e = 0; e < VEC; e += 2) {
+        cmt = vmax3(cmt, vt[h][e], vt[h][e + 1]);
+        if (PAIR) cmd = vmax3(cmd, vd[h][e], vd[h][e + 1]);
+      }
+  };
+  // new reference points for the lanes whose chunk maximum passed theirs by
+  // more than kSlack; the sums are rescaled to them
+  auto rescale = [&](bool up_t, bool up_d, Acc cmt, Acc cmd) {
+    const Acc nt = up_t ? cmt : S.mt;
+    const Acc nd = up_d ? cmd : S.md;
+    const Acc ntL = nt * L, ndL = nd * L;
+    const Acc ft = fast_exp2(S.mtL - ntL);
+    const Acc fd = fast_exp2(S.mdL - ndL);
+    const Acc fz = NEEDZ ? fast_exp2(Acc(p.omt_f) * (S.mtL - ntL) + Acc(p.tau_f) * (S.mdL - ndL))
+                         : Acc(1);
+    if constexpr (sizeof(Acc) == 4) {
+      S.pst = mul2(S.pst, pk2(ft, ft));
+      if (PAIR) S.psd = mul2(S.psd, pk2(fd, fd));
+      if (NEEDZ) S.psz = mul2(S.psz, pk2(fz, fz));
+    } else {
+      S.st *= ft;
+      if (PAIR) S.sd *= fd;
+      if (NEEDZ) S.sz *= fz;
     }
-  if (PAIR) {
+    S.mt = nt;
+    S.md = nd;
+    S.mtL = ntL;
+    S.mdL = ndL;
+  };
+  auto exps = [&]() {
+#pragma unroll
+    for (int h = 0; h < kVecs; ++h) {
+      if constexpr (sizeof(Acc) == 4)
+        exp_acc<PAIR, NEEDZ, VEC>(vt[h], vd[h], S, p);
+      else
+        exp_sums<PAIR, NEEDZ, VEC>(vt[h], vd[h], S, p);
+    }
+  };
+  // top-m bookkeeping: one warp max per row (the key of block (chunk, warp))
+  // against the row's running bound; the rare blocks that reach it are captured
+  auto topm = [&](Acc cmt, Acc cmd) {
+    if (!PAIR) return;
     S.diff |= diff;
     const int lt = fkey(cmt), ld = fkey(cmd);
     const int bt = warp_max_key(lt);
@@ -523,28 +617,52 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
     if (bt >= th0 || bd >= th1) {
 #endif
       TR_START(tcap);
-      if (bt >= th0) capture_row<In, TAIL>(sl, 0, lt, th0, vt, starget, c, tid, lane, p, trl);
-      if (bd >= th1) capture_row<In, TAIL>(sl, 1, ld, th1, vd, sdraft, c, tid, lane, p, trl);
+      if (bt >= th0) capture_row<In, TAIL>(sl, 0, lt, th0, starget, c, tid, lane, p, trl);
+      if (bd >= th1) capture_row<In, TAIL>(sl, 1, ld, th1, sdraft, c, tid, lane, p, trl);
       TR_ADD(trl, kTrCapCycles, tcap);
     }
+  };
+
+#ifndef DSDV_ORDER
+#define DSDV_ORDER 1
+#endif
+  load();
+  Acc cmt, cmd;
+  if (sizeof(Acc) == 8 || c == 0 || DSDV_ORDER < 2) {
+    // max first: the item's first chunk sets the reference points
+    chunk_max(cmt, cmd);
+    if (DSDV_ORDER == 0) topm(cmt, cmd);
+    const bool up_t = cmt > S.mt + Acc(kSlack);
+    const bool up_d = PAIR && (cmd > S.md + Acc(kSlack));
+    if (__any_sync(0xffffffffu, up_t || up_d)) rescale(up_t, up_d, cmt, cmd);
+    exps();
+    if (DSDV_ORDER != 0) topm(cmt, cmd);
+    return;
   }
-  // lazy online max: one warp vote per chunk, rarely taken
+  // exponentials first, against the current reference points
+  const f32x2 s0t = S.pst, s0d = S.psd, s0z = S.psz;
+  exps();
+  chunk_max(cmt, cmd);
+  topm(cmt, cmd);
   const bool up_t = cmt > S.mt + Acc(kSlack);
   const bool up_d = PAIR && (cmd > S.md + Acc(kSlack));
   if (__any_sync(0xffffffffu, up_t || up_d)) {
-    const Acc nt = up_t ? cmt : S.mt;
-    const Acc nd = up_d ? cmd : S.md;
-    const Acc ntL = nt * L, ndL = nd * L;
-    if (NEEDZ) S.sz *= fast_exp2(Acc(p.omt_f) * (S.mtL - ntL) + Acc(p.tau_f) * (S.mdL - ndL));
-    S.st *= fast_exp2(S.mtL - ntL);
-    if (PAIR) S.sd *= fast_exp2(S.mdL - ndL);
-    S.mt = nt;
-    S.md = nd;
-    S.mtL = ntL;
-    S.mdL = ndL;
+    const bool over = cmt > S.mt + Acc(kGuard) || (PAIR && cmd > S.md + Acc(kGuard));
+    if (__any_sync(0xffffffffu, over)) {
+      // rare: this chunk may have overflowed against the old reference; fold
+      // it again from the resident stage against the new one
+      if constexpr (sizeof(Acc) == 4) {
+        S.pst = s0t;
+        S.psd = s0d;
+        S.psz = s0z;
+      }
+      rescale(up_t, up_d, cmt, cmd);
+      load();
+      exps();
+    } else {
+      rescale(up_t, up_d, cmt, cmd);
+    }
   }
-#pragma unroll
-  for (int h = 0; h < kVecs; ++h) exp_sums<PAIR, NEEDZ, VEC>(vt[h], vd[h], S, p);
 }
 
 // Sample item: per-tile fp64 sums of the residual / bonus weights. Tile
@@ -711,6 +829,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     Slot<Acc> &sl = sm.slot[s];
     if (kind == kRegular) {
       const Acc omt = Acc(p.omt_f), tau = Acc(p.tau_f);
+      S.flush();
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         const Acc mt2 = __shfl_xor_sync(0xffffffffu, S.mt, off);
@@ -1376,10 +1495,17 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
     const int si = n % kSlots;
     TR_START(tw);
     // while the compute warps fold this slot's item, keep its top-m bound tight
+#ifdef DSDV_EPI_BLOCK
+    mbar_wait(&sm.part_full[si], (n / kSlots) & 1);
+#else
+#ifndef DSDV_EPI_SLEEP
+#define DSDV_EPI_SLEEP 64
+#endif
     while (!mbar_test(&sm.part_full[si], (n / kSlots) & 1)) {
       refresh_theta(sm.slot[si], M, lane);
-      __nanosleep(64);
+      __nanosleep(DSDV_EPI_SLEEP);
     }
+#endif
     TR_ADD(trl, kTrEpiWaitFull, tw);
     TR_START(tx);
     Slot<Acc> &sl = sm.slot[si];

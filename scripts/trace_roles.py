@@ -49,7 +49,9 @@ def run_window():
     if SHARD:
         sv.stats(ds, ts, tokens, p, V, lo, n)
     else:
-        run_window()
+        v.verify(draft, target, tokens, p, vocab=V, out=out)
+
+
 for w in range(3):
     p.window = w
     run_window()
