@@ -391,9 +391,8 @@ def run_sharded(args, rank, world, local_rank):
     ms_max = float(ms_t.item())
     mean_k = float(out.accepted_count.float().mean().item())
     committed = float((out.accepted_count.float() + 1).sum().item())
-    bad = int((out.status != 0).sum().item())
-    if args.exchange == "peer":
-        
+    bad = int((out.status != 0).sum().item())  # includes peer flag-round timeouts (DSDV_E_NCCL)
+
     # e2e: this rank's slice and the tokens from pinned host memory, results back
     draft_h, target_h, tokens_h = (draft.cpu().pin_memory(), target.cpu().pin_memory(),
                                    tokens.cpu().pin_memory())
