@@ -247,6 +247,51 @@ def run_ours(args, rank, world, local_rank):
     committed = float((out.accepted_count.float() + 1).sum().item())
     timed_k = out.accepted_count.cpu().numpy()
 
+    # ---- early exit (dsdv_verify_early_exit): rows past each sequence's first
+    # rejection are not streamed; same k / extra tokens. Its roofline counts the
+    # rows the reference actually needs, never the full window's bytes.
+    early = None
+    if world == 1:
+        def estep(w):
+            p.window = w
+            ver.verify(draft, target, tokens, p, vocab=V, out=out, stream=stream,
+                       early_exit=True)
+        for w in range(args.warmup):
+            estep(10_000 + w)
+        ver.sync(p, out, batch=B, vocab=V)
+        ver.streamed_bytes(reset=True)
+        torch.cuda.synchronize(device)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for k in range(args.steps):
+            estep(k)
+        g1.record(stream)
+        torch.cuda.synchronize(device)
+        ems = g0.elapsed_time(g1) / args.steps
+        streamed = ver.streamed_bytes(reset=True) / args.steps
+        # rows the reference needs, per timed window (k differs per window index)
+        need_rows = 0
+        ks = []
+        for k in range(args.steps):
+            estep(k)
+            kk = out.accepted_count.cpu()
+            ks.append(kk)
+            need_rows += int(torch.where(kk < GAMMA, 2 * (kk + 1), 2 * GAMMA + 1).sum())
+        need_bytes = need_rows * V * 2 / args.steps
+        ek = torch.stack(ks)
+        early = {"value": B * GAMMA / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems,
+                 "mean_accepted_k": float(ek.float().mean()),
+                 "same_k_as_full_window": bool(torch.equal(ek[-1], out.accepted_count.cpu())),
+                 "required_bytes_per_window": need_bytes, "streamed_bytes_per_window": streamed,
+                 "roofline": {"bound": "hbm", "achieved": need_bytes / (ems * 1e-3) / 1e9,
+                              "peak": measured_peaks().get("hbm_gbs", 6650.0), "unit": "GB/s",
+                              "frac": need_bytes / (ems * 1e-3) / 1e9 /
+                              measured_peaks().get("hbm_gbs", 6650.0),
+                              "note": "required bytes = row pairs 0..k (k < gamma) or all gamma "
+                                      "pairs + target row gamma (k = gamma), each read once "
+                                      "(SPEC.md:244); streamed bytes include the extra-draw "
+                                      "re-reads and rows in flight when a rejection landed"}}
+
     # ---- e2e: host buffers through the public API, copies inside the timed region
     draft_h = draft.cpu().pin_memory()
     target_h = target.cpu().pin_memory()
@@ -334,6 +379,8 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = cpu
     if parity is not None:
         line["parity"] = parity
+    if early is not None:
+        line["early_exit"] = early
     print(json.dumps(line), flush=True)
 
 

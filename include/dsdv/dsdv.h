@@ -144,6 +144,23 @@ dsdv_status dsdv_verify(dsdv_ctx *ctx, const dsdv_params *params, const void *dr
                         const void *target_logits, const int32_t *draft_tokens,
                         const dsdv_outputs *out, void *stream);
 
+/* dsdv_verify with early exit (verifier.cpp:250): a sequence's
+ * positions past its first rejection are never evaluated by the reference, so
+ * their rows are not streamed once the rejection is known (items not yet
+ * started are skipped, items in flight stop at their next chunk), nor is
+ * target row gamma unless every position was accepted. Same per-sequence
+ * results (k, extra token, key count, status) as dsdv_verify; per-position
+ * outputs are defined up to and including the first rejection only. */
+dsdv_status dsdv_verify_early_exit(dsdv_ctx *ctx, const dsdv_params *params,
+                                   const void *draft_logits, const void *target_logits,
+                                   const int32_t *draft_tokens, const dsdv_outputs *out,
+                                   void *stream);
+
+/* Logit bytes the fused verifier's producers copied from global memory since
+ * the last reset (accumulated over launches on this context). Synchronous:
+ * waits for the device. reset != 0 clears the counter after reading. */
+dsdv_status dsdv_streamed_bytes(dsdv_ctx *ctx, int reset, uint64_t *bytes);
+
 /* Statistics and accept probabilities for every position, no draws. Fills the
  * per-position outputs, records, and status[B] (first error position, as the
  * reference would raise it walking left to right with all positions evaluated). */

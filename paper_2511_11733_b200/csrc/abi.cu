@@ -58,6 +58,8 @@ struct dsdv_ctx {
   unsigned int *flags = nullptr;  // [positions]
   int2 *slots = nullptr;          // [positions]
   unsigned int *done = nullptr;   // [sequences]
+  unsigned long long *stop = nullptr;      // [sequences] early-exit stop keys
+  unsigned long long *streamed = nullptr;  // logit bytes copied by the fused kernel
   unsigned long long *trace = nullptr;  // DSDV_TRACE builds: [grid][kTraceWords]
   size_t flags_cap = 0;
   size_t done_cap = 0;
@@ -107,6 +109,10 @@ dsdv_status ensure_scratch(dsdv_ctx *ctx, size_t n_positions, size_t n_sequences
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(counters)");
     e = cudaMemset(ctx->counters, 0, 2 * sizeof(unsigned int));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemset(counters)");
+    e = cudaMalloc(&ctx->streamed, sizeof(unsigned long long));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(streamed)");
+    e = cudaMemset(ctx->streamed, 0, sizeof(unsigned long long));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemset(streamed)");
   }
   if (n_positions > ctx->flags_cap) {
     if (ctx->flags) cudaFree(ctx->flags);
@@ -117,8 +123,7 @@ dsdv_status ensure_scratch(dsdv_ctx *ctx, size_t n_positions, size_t n_sequences
     if (ctx->slots) cudaFree(ctx->slots);
     e = cudaMalloc(&ctx->slots, n_positions * sizeof(int2));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(slots)");
-    ctx->flags_cap = n_positions;
-    ctx->epoch = 0;
+    ctx->flags_cap = n_positions;  // zeroed words carry epoch 0, never a live one
   }
   if (n_sequences > ctx->done_cap) {
     if (ctx->done) cudaFree(ctx->done);
@@ -126,6 +131,11 @@ dsdv_status ensure_scratch(dsdv_ctx *ctx, size_t n_positions, size_t n_sequences
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(done)");
     e = cudaMemset(ctx->done, 0, n_sequences * sizeof(unsigned int));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemset(done)");
+    if (ctx->stop) cudaFree(ctx->stop);
+    e = cudaMalloc(&ctx->stop, n_sequences * sizeof(unsigned long long));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(stop)");
+    e = cudaMemset(ctx->stop, 0, n_sequences * sizeof(unsigned long long));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemset(stop)");
     ctx->done_cap = n_sequences;
   }
   return DSDV_OK;
@@ -192,7 +202,7 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
                       const void *target, const int32_t *tokens, const dsdv_outputs *out,
                       void *stream, bool stats_only, double *topv = nullptr,
                       int32_t *topi = nullptr, int npeer = 0,
-                      const long long *peer_delta = nullptr) {
+                      const long long *peer_delta = nullptr, bool early_exit = false) {
   const bool partial = topv != nullptr;
   if (!ctx) return DSDV_E_INVARIANT;
   DevParams d;
@@ -200,6 +210,7 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   if (st != DSDV_OK) return st;
   d.stats_only = stats_only ? 1 : 0;
   d.partial = partial ? 1 : 0;
+  d.early_exit = early_exit ? 1 : 0;
   if (partial && !topi)
     return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_stats: top lists are required");
   if (!draft || !target || !tokens || !out)
@@ -219,7 +230,10 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   if (st != DSDV_OK) return st;
   ctx->epoch = (ctx->epoch + 1) & 0x0fffffffu;
   if (ctx->epoch == 0) {
+    // wrap-around: no word may still carry a recycled epoch
     cudaMemsetAsync(ctx->flags, 0, ctx->flags_cap * sizeof(unsigned int), (cudaStream_t)stream);
+    cudaMemsetAsync(ctx->stop, 0, ctx->done_cap * sizeof(unsigned long long),
+                    (cudaStream_t)stream);
     ctx->epoch = 1;
   }
   d.epoch = ctx->epoch;
@@ -229,6 +243,8 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   s.flags = ctx->flags;
   s.slots = ctx->slots;
   s.done = ctx->done;
+  s.stop = ctx->stop;
+  s.streamed = ctx->streamed;
   s.trace = nullptr;
 #ifdef DSDV_TRACE
   if (!ctx->trace) {
@@ -295,6 +311,8 @@ dsdv_status dsdv_destroy(dsdv_ctx *ctx) {
   if (ctx->flags) cudaFree(ctx->flags);
   if (ctx->slots) cudaFree(ctx->slots);
   if (ctx->done) cudaFree(ctx->done);
+  if (ctx->stop) cudaFree(ctx->stop);
+  if (ctx->streamed) cudaFree(ctx->streamed);
   if (ctx->trace) cudaFree(ctx->trace);
   delete ctx;
   return DSDV_OK;
@@ -379,6 +397,29 @@ dsdv_status dsdv_verify(dsdv_ctx *ctx, const dsdv_params *params, const void *dr
                         const void *target_logits, const int32_t *draft_tokens,
                         const dsdv_outputs *out, void *stream) {
   return run_fused(ctx, params, draft_logits, target_logits, draft_tokens, out, stream, false);
+}
+
+dsdv_status dsdv_verify_early_exit(dsdv_ctx *ctx, const dsdv_params *params,
+                                   const void *draft_logits, const void *target_logits,
+                                   const int32_t *draft_tokens, const dsdv_outputs *out,
+                                   void *stream) {
+  return run_fused(ctx, params, draft_logits, target_logits, draft_tokens, out, stream, false,
+                   nullptr, nullptr, 0, nullptr, true);
+}
+
+dsdv_status dsdv_streamed_bytes(dsdv_ctx *ctx, int reset, uint64_t *bytes) {
+  if (!ctx || !bytes) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  unsigned long long v = 0;
+  e = cudaMemcpy(&v, ctx->streamed, sizeof(v), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "dsdv_streamed_bytes");
+  *bytes = (uint64_t)v;
+  if (reset) {
+    e = cudaMemset(ctx->streamed, 0, sizeof(unsigned long long));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "dsdv_streamed_bytes reset");
+  }
+  return DSDV_OK;
 }
 
 dsdv_status dsdv_window_stats(dsdv_ctx *ctx, const dsdv_params *params, const void *draft_logits,

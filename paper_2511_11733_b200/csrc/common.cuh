@@ -46,6 +46,7 @@ struct DevParams {
   int stats_only;   // 1: dsdv_window_stats (no draws, no waits, no sampling)
   int partial;      // 1: dsdv_shard_stats (partial records of a vocabulary slice only)
   int need_z;       // 0 < tau < 1
+  int early_exit;   // 1: dsdv_verify_early_exit (rows past a sequence's first rejection are skipped)
   float tau_f, omt_f;
   double tau, ratio_limit, gap_limit, overlap_floor, eps_u, eps_lambda;
   uint64_t seed, window;
@@ -73,6 +74,8 @@ struct DevScratch {
   int2 *slots;               // [B][gamma+1] extra-token draws (token, status | near << 8)
   unsigned int *done;        // [B] items finished this window (reset by the finaliser)
   unsigned long long *trace; // [grid][kTraceWords] cycle counters (DSDV_TRACE builds only)
+  unsigned long long *stop;  // [B] first known stop position, epoch << 8 | (255 - j) (atomicMax)
+  unsigned long long *streamed;  // logit bytes the producers copied (accumulated across launches)
 };
 constexpr int kTraceWords = 28;
 

@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <mutex>
 
 #include "common.cuh"
 #include "sample.cuh"
@@ -96,11 +97,22 @@ struct Ring {
 constexpr int kMaxTiles = 1024;      // blocks per slot: (chunk, warp), kVecs*32*VEC ids each
 constexpr int kAreaBytes = 8 * kMaxTiles;  // per-slot block maxima (2 x int), or sample tiles (double)
 constexpr int kCap = 256;            // captured top-m candidates per row and item
-constexpr int kReq = 16;             // sample-request queue
+// Sample-request queue. Bound: a request is outstanding from its posting until
+// the epilogue finishes its sample item. Stream items the producer issued but
+// the epilogue has not finished are at most kSlots + kStages (slot reuse and
+// the ring), and between two item boundaries of the producer (where it takes
+// every pending request) the epilogue finishes at most that many regular
+// items, so at most 2 (kSlots + kStages) + kEW < 32 requests are outstanding.
+#ifndef DSDV_KREQ
+#define DSDV_KREQ 32
+#endif
+constexpr int kReq = DSDV_KREQ;
 constexpr float kSlack = 8.0f;       // lazy max: rescale when a value exceeds m by this much
 constexpr float kFloorM = -1e30f;    // finite "empty" max (keeps (v - m) free of inf - inf)
 
-enum ItemKind : int { kRegular = 0, kSample = 1 };
+enum ItemKind : int { kRegular = 0, kSample = 1, kAborted = 2 };
+// StageMeta::kr bit 8: an early-exit abort stage (no data; ends its item)
+constexpr int kAbortBit = 1 << 8;
 
 // Optional cycle accounting per CTA (compile with -DDSDV_TRACE; see
 // scripts/trace_roles.py): where each warp role spends its time.
@@ -143,7 +155,8 @@ struct alignas(16) StageMeta {  // one LDS.128 per chunk
   int n;      // CTA-local stream index (slot = n % kSlots)
   int kr;     // kind (kRegular / kSample) | sample request index << 1
   __device__ __forceinline__ int kind() const { return kr & 1; }
-  __device__ __forceinline__ int req() const { return kr >> 1; }
+  __device__ __forceinline__ int req() const { return (kr >> 1) & 127; }
+  __device__ __forceinline__ bool abort() const { return (kr & kAbortBit) != 0; }
 };
 
 template <class Acc>
@@ -705,7 +718,7 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
   if (lane == 0) tiles[chunk * kCW + warp] = ts;
 }
 
-template <class In, bool NEEDZ>
+template <class In, bool NEEDZ, bool EE>
 __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
                              const In *__restrict__ draft, const In *__restrict__ target, int tid,
                              unsigned long long *tr) {
@@ -777,7 +790,10 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     }
     if (false) {
 #else
-    if (kind == kRegular) {
+    if (EE && md.abort()) {
+      // early exit: the item's sequence already stopped at an earlier position;
+      // no data, the item ends here
+    } else if (kind == kRegular) {
 #endif
       // a short last chunk is masked element by element unless the producer
       // padded it with -inf (pad_tail)
@@ -866,7 +882,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
     }
     if (tid == 0) {
       sl.item = md.item;
-      sl.kind = kind;
+      sl.kind = (EE && md.abort()) ? kAborted : kind;
       sl.req = md.req();
     }
     __syncwarp();
@@ -1227,6 +1243,21 @@ __device__ __forceinline__ uint32_t flag_word(const DevParams &p, const PosEval 
   return (p.epoch << 4) | (ev.near << 3) | (ev.key << 2) | outcome;
 }
 
+// Early exit (positions after the first rejection are never
+// evaluated): the smallest known stopping position of sequence b this launch.
+__device__ __forceinline__ unsigned long long stop_key(const DevParams &p, int j) {
+  return ((unsigned long long)p.epoch << 8) | (unsigned long long)(255 - j);
+}
+__device__ __forceinline__ void publish_stop(const DevScratch &s, const DevParams &p, int b, int j) {
+  atomicMax(s.stop + b, stop_key(p, j));
+}
+// true when an earlier position than j is known to end sequence b's window
+__device__ __forceinline__ bool stopped_before(const DevScratch &s, const DevParams &p, int b,
+                                               int j) {
+  const unsigned long long w = *(volatile const unsigned long long *)(s.stop + b);
+  return (w >> 8) == (unsigned long long)p.epoch && 255 - (int)(w & 0xffu) < j;
+}
+
 // The last item of sequence b to finish commits the round (verifier.cpp:223-256).
 __device__ void finalize_sequence(const DevOut &o, const DevScratch &s, const DevParams &p, int b) {
   const int G1 = p.gamma + 1;
@@ -1480,7 +1511,7 @@ __device__ __noinline__ void write_partial(const DevOut &o, const DevParams &p, 
   // fences at system scope and releases the arrival flags)
 }
 
-template <class In>
+template <class In, bool EE>
 __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
                               const In *__restrict__ draft, const In *__restrict__ target,
                               const int32_t *__restrict__ tokens, const DevOut &o,
@@ -1517,7 +1548,15 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
     const In *rd = draft + ((size_t)b * p.gamma + (pair ? j : 0)) * (size_t)p.stride;
     int2 *slotp = s.slots + (size_t)b * G1 + j;
 
-    if (sl.kind == kRegular) {
+    if (EE && sl.kind == kAborted) {
+      // early exit: an item cut short after its sequence stopped earlier
+      if (pair) reset_capture(sl, lane);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sm.part_empty[si]);
+        complete_item(o, s, p, b);
+      }
+    } else if (sl.kind == kRegular) {
       double mrg[7];
       int diff = 0;
       merge_partials(sl, p, lane, mrg, diff);
@@ -1568,6 +1607,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       if (lane == 0) {
         if (pair) decide_position(p, b, j, ev);
         write_position(o, p, b, j, pair, ev);
+        if (EE && pair && (ev.err || !ev.accepted)) publish_stop(s, p, b, j);  // positions past j are never needed (verifier.cpp:250)
         if (!p.stats_only) {
           const unsigned int *fl = s.flags + (size_t)b * G1;
           bool stopped_before = false;  // an earlier position already ends the window
@@ -1593,12 +1633,20 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
             else
               want = 2;
           }
-          if (want) {
+          if (want && vload(&sm.req_tail) - vload(&sm.req_done) >= kReq - kEW) {
+            // cannot happen by the bound above; fail the sequence, never the context
+            *slotp = make_int2(-1, DSDV_E_UNSUPPORTED);
+            if (pair) {
+              __threadfence();
+              st_release(s.flags + (size_t)b * G1 + j, flag_word(p, ev, kOutError));
+            }
+            complete_item(o, s, p, b);
+            want = 0;
+          } else if (want) {
             // the flag of a drawing position is published once its draw lands;
             // stash it in the slot until then
             if (pair) *slotp = make_int2(-2, (int)flag_word(p, ev, kOutRejected));
             const int t = atomicAdd(&sm.req_tail, 1);
-            if (t - vload(&sm.req_done) >= kReq) __trap();  // queue bound
             Request<Acc> &rq = sm.req[t % kReq];
             rq.item = item;
             rq.rows = want == 1 ? 2 : 1;
@@ -1696,16 +1744,34 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
 }
 
 // ------------------------------------------------------------------ producer warp
-template <class In, class Acc = typename InTraits<In>::Acc>
+template <class In, bool EE, class Acc = typename InTraits<In>::Acc>
 __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
                                             const In *rd, bool two, int item, int kind, int n,
                                             int req, int n_chunks, int nlocal, bool pad, int &stage,
-                                            uint32_t &phase, unsigned long long *tr) {
+                                            uint32_t &phase, unsigned long long *tr,
+                                            unsigned long long &copied, const DevScratch &sx,
+                                            const DevParams &pp, int b, int j) {
   constexpr int CH = kRowBytes / (int)sizeof(In);
   for (int c = 0; c < n_chunks; ++c) {
     TR_START(tw);
     mbar_wait_spin(&sm.empty[stage], phase ^ 1);
     TR_ADD(tr, kTrProdWaitEmpty, tw);
+    if (EE && kind == kRegular && j > 0 && c > 0 && stopped_before(sx, pp, b, j)) {
+      // early exit: the sequence stopped at an earlier position while this
+      // item streamed; an empty stage ends the item
+      StageMeta m;
+      m.item = item;
+      m.chunk = n_chunks - 1;
+      m.n = n;
+      m.kr = kind | (req << 1) | kAbortBit;
+      sm.meta[stage] = m;
+      mbar_arrive(&sm.full[stage]);
+      if (++stage == Smem<Acc>::kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+      return;
+    }
     StageMeta m;
     m.item = item;
     m.chunk = c;
@@ -1715,6 +1781,7 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
     const int rem = nlocal - c * CH;
     const int elems = rem < CH ? rem : CH;
     const uint32_t bytes = ((uint32_t)(elems * (int)sizeof(In)) + 15u) & ~15u;
+    copied += two ? 2u * bytes : bytes;
 #ifdef DSDV_TIMELINE
     if (tr && blockIdx.x == 0) {
       unsigned long long *tl = tr + 512 * kTraceWords;
@@ -1748,11 +1815,12 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
   }
 }
 
-template <class In>
+template <class In, bool EE>
 __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
                               const In *__restrict__ draft, const In *__restrict__ target,
-                              const DevScratch &s, unsigned long long *tr) {
+                              const DevOut &o, const DevScratch &s, unsigned long long *tr) {
   const int G1 = p.gamma + 1;
+  unsigned long long copied = 0;
   int stage = 0;
   uint32_t phase = 0;
   int n = 0, next = -1;
@@ -1770,8 +1838,8 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       const int j = item / p.B, b = item - j * p.B;
       const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
       const In *rd = draft + ((size_t)b * p.gamma + (j < p.gamma ? j : 0)) * (size_t)p.stride;
-      stream_rows<In>(sm, rt, rd, two, item, kSample, n, r, p.n_chunks, p.vocab_local, false, stage,
-                      phase, tr);
+      stream_rows<In, EE>(sm, rt, rd, two, item, kSample, n, r, p.n_chunks, p.vocab_local, false, stage,
+                      phase, tr, copied, s, p, b, j);
       TR_INC(tr, kTrProdSamples);
       ++n;
       vstore(&sm.req_head, head + 1);
@@ -1786,10 +1854,16 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
         next = (int)atomicAdd(s.ticket, 1u);
         const int j = item / p.B, b = item - j * p.B;  // position-major order
         const bool pair = j < p.gamma;
+        if (EE && j > 0 && stopped_before(s, p, b, j)) {
+          // early exit: an earlier position already ends this sequence's window
+          // (verifier.cpp:250); the item is never streamed, only counted
+          complete_item(o, s, p, b);
+          continue;
+        }
         const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
         const In *rd = draft + ((size_t)b * p.gamma + (pair ? j : 0)) * (size_t)p.stride;
-        stream_rows<In>(sm, rt, rd, pair, item, kRegular, n, 0, p.n_chunks, p.vocab_local,
-                        pad_tail<In>(p), stage, phase, tr);
+        stream_rows<In, EE>(sm, rt, rd, pair, item, kRegular, n, 0, p.n_chunks, p.vocab_local,
+                        pad_tail<In>(p), stage, phase, tr, copied, s, p, b, j);
         TR_INC(tr, kTrProdItems);
         ++n;
         continue;
@@ -1808,6 +1882,7 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
     TR_ADD(tr, kTrProdDrain, td);
   }
   // end of stream
+  if (s.streamed) atomicAdd(s.streamed, copied);
   mbar_wait(&sm.empty[stage], phase ^ 1);
   StageMeta m;
   m.item = -1;
@@ -1819,7 +1894,7 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
 }
 
 // ------------------------------------------------------------------ kernel
-template <class In>
+template <class In, bool EE>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_verify_kernel(const __grid_constant__ DevParams p, const In *__restrict__ draft,
                         const In *__restrict__ target, const int32_t *__restrict__ tokens,
@@ -1850,9 +1925,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   if (warp == kProdWarp) {
-    if (lane == 0) producer_loop<In>(sm, p, draft, target, s, tr);
+    if (lane == 0) producer_loop<In, EE>(sm, p, draft, target, o, s, tr);
   } else if (warp >= kEpiWarp) {
-    epilogue_loop<In>(sm, p, draft, target, tokens, o, s, warp - kEpiWarp, lane, tr);
+    epilogue_loop<In, EE>(sm, p, draft, target, tokens, o, s, warp - kEpiWarp, lane, tr);
     if (lane == 0 && atomicAdd(&sm.epi_exit, 1) == kEW - 1) {
       TR_ADD(tr, kTrKernel, tk);
       // last CTA out re-arms the work counters for the next launch
@@ -1866,51 +1941,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     if (p.need_z)
-      compute_loop<In, true>(sm, p, draft, target, tid, tr);
+      compute_loop<In, true, EE>(sm, p, draft, target, tid, tr);
     else
-      compute_loop<In, false>(sm, p, draft, target, tid, tr);
+      compute_loop<In, false, EE>(sm, p, draft, target, tid, tr);
   }
 }
 
 }  // namespace fz
 
 // ------------------------------------------------------------------ launch
+template <class In, bool EE>
+cudaError_t launch_fused_t(const DevParams &q, const void *draft, const void *target,
+                           const int32_t *tokens, const DevOut &o, const DevScratch &s,
+                           cudaStream_t stream, int *grid_out) {
+  using Acc = typename InTraits<In>::Acc;
+  const size_t smem = sizeof(fz::Smem<Acc>);
+  // occupancy is a property of (kernel, device): one query per device, the
+  // cache guarded for concurrent host threads (sweep workers)
+  static std::mutex mu;
+  static int grid_cap[64] = {0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  int grid;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (grid_cap[dev] == 0) {
+      e = cudaFuncSetAttribute(fz::fused_verify_kernel<In, EE>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      int per_sm = 0, sms = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fz::fused_verify_kernel<In, EE>,
+                                                        fz::kThreads, smem);
+      if (e != cudaSuccess) return e;
+      e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return e;
+      if (per_sm < 1) return cudaErrorInvalidConfiguration;
+      grid_cap[dev] = per_sm * sms;
+    }
+    grid = grid_cap[dev];
+  }
+  if (grid > q.n_items) grid = q.n_items;
+  if (grid_out) *grid_out = grid;
+  fz::fused_verify_kernel<In, EE><<<grid, fz::kThreads, smem, stream>>>(
+      q, (const In *)draft, (const In *)target, tokens, o, s);
+  return cudaGetLastError();
+}
+
 template <class In>
 cudaError_t launch_fused(const DevParams &p, const void *draft, const void *target,
                          const int32_t *tokens, const DevOut &o, const DevScratch &s,
                          cudaStream_t stream, int *grid_out) {
-  using Acc = typename InTraits<In>::Acc;
   constexpr int CH = fz::kRowBytes / (int)sizeof(In);
   DevParams q = p;
   q.n_chunks = (p.vocab_local + CH - 1) / CH;
   const int ntiles = q.n_chunks * fz::kCW;
   if (ntiles > fz::kMaxTiles || 8 * q.n_chunks * fz::kCW > fz::kAreaBytes)
     return cudaErrorInvalidValue;
-  const size_t smem = sizeof(fz::Smem<Acc>);
-  // occupancy is a property of (kernel, device): query once per device
-  static int cached_device = -1, cached_grid_cap = 0;
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (cached_device != dev) {
-    e = cudaFuncSetAttribute(fz::fused_verify_kernel<In>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fz::fused_verify_kernel<In>,
-                                                      fz::kThreads, smem);
-    if (e != cudaSuccess) return e;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    cached_grid_cap = per_sm * sms;
-    cached_device = dev;
-  }
-  int grid = cached_grid_cap;
-  if (grid > q.n_items) grid = q.n_items;
-  if (grid_out) *grid_out = grid;
-  fz::fused_verify_kernel<In><<<grid, fz::kThreads, smem, stream>>>(
-      q, (const In *)draft, (const In *)target, tokens, o, s);
-  return cudaGetLastError();
+  return q.early_exit ? launch_fused_t<In, true>(q, draft, target, tokens, o, s, stream, grid_out)
+                      : launch_fused_t<In, false>(q, draft, target, tokens, o, s, stream, grid_out);
 }
 
 // Vocabulary limit of the fused kernel for a dtype (per-slot block maxima, or

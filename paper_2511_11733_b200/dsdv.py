@@ -75,6 +75,9 @@ def _load() -> C.CDLL:
         "dsdv_abi_version": (C.c_int, []),
         "dsdv_validate": (st, [vp, C.POINTER(_Params)]),
         "dsdv_verify": (st, [vp, C.POINTER(_Params), vp, vp, vp, C.POINTER(_Outputs), vp]),
+        "dsdv_verify_early_exit": (st, [vp, C.POINTER(_Params), vp, vp, vp, C.POINTER(_Outputs),
+                                        vp]),
+        "dsdv_streamed_bytes": (st, [vp, C.c_int, C.POINTER(C.c_uint64)]),
         "dsdv_window_stats": (st, [vp, C.POINTER(_Params), vp, vp, vp, C.POINTER(_Outputs), vp]),
         "dsdv_sample_extra": (st, [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp, vp]),
         "dsdv_draft_sample": (st, [vp, C.POINTER(_Params), vp, vp, vp]),
@@ -110,7 +113,12 @@ def _load() -> C.CDLL:
                                       vp]),
     }
     for name, (res, args) in sigs.items():
-        fn = getattr(lib, name)
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            if LIB_PATH.name == "libdsdv.so":
+                raise  # the product library must export the whole ABI
+            continue  # an older development build (DSDV_LIB)
         fn.restype = res
         fn.argtypes = args
     return lib
@@ -118,7 +126,7 @@ def _load() -> C.CDLL:
 
 LIB = _load()
 EXPORTED = ("dsdv_create", "dsdv_destroy", "dsdv_last_error", "dsdv_abi_version", "dsdv_validate",
-            "dsdv_verify", "dsdv_window_stats", "dsdv_sample_extra", "dsdv_draft_sample",
+            "dsdv_verify", "dsdv_verify_early_exit", "dsdv_streamed_bytes", "dsdv_window_stats", "dsdv_sample_extra", "dsdv_draft_sample",
             "dsdv_sync", "dsdv_uniform", "dsdv_synth_logits", "dsdv_launch_count",
             "dsdv_shard_stats", "dsdv_shard_merge", "dsdv_shard_sample", "dsdv_mix_rows",
             "dsdv_spin", "dsdv_draft_sample_temperature", "dsdv_dev_alloc", "dsdv_dev_free",
@@ -271,16 +279,25 @@ class Verifier:
 
     def verify(self, draft: torch.Tensor, target: torch.Tensor, tokens: torch.Tensor,
                p: VerifyParams, vocab: int | None = None, out: WindowResult | None = None,
-               stream: torch.cuda.Stream | None = None, per_position: bool = True) -> WindowResult:
-        """dsdv_verify: one fused window for every sequence (asynchronous)."""
+               stream: torch.cuda.Stream | None = None, per_position: bool = True,
+               early_exit: bool = False) -> WindowResult:
+        """dsdv_verify (or dsdv_verify_early_exit): one fused window for every
+        sequence (asynchronous)."""
         vocab = draft.shape[-1] if vocab is None else vocab
         cp = self.params(p, draft, target, tokens, vocab)
         if out is None:
             out = WindowResult.allocate(cp.batch, cp.gamma, draft.device, per_position)
         s = (stream or torch.cuda.current_stream(draft.device)).cuda_stream
-        self._check(LIB.dsdv_verify(self._h, C.byref(cp), draft.data_ptr(), target.data_ptr(),
-                                    tokens.data_ptr(), C.byref(out._c), s))
+        fn = LIB.dsdv_verify_early_exit if early_exit else LIB.dsdv_verify
+        self._check(fn(self._h, C.byref(cp), draft.data_ptr(), target.data_ptr(),
+                       tokens.data_ptr(), C.byref(out._c), s))
         return out
+
+    def streamed_bytes(self, reset: bool = False) -> int:
+        """dsdv_streamed_bytes: logit bytes copied by the fused kernel (syncs)."""
+        v = C.c_uint64(0)
+        self._check(LIB.dsdv_streamed_bytes(self._h, 1 if reset else 0, C.byref(v)))
+        return int(v.value)
 
     def window_stats(self, draft, target, tokens, p: VerifyParams, vocab: int | None = None,
                      out: WindowResult | None = None, stream=None) -> WindowResult:

@@ -147,3 +147,35 @@ def test_batched_error_statuses(verifier, oracle, dtype):
     with pytest.raises(DsdvError) as ei:
         verifier.sync(p, o, batch=B, vocab=V)
     assert ei.value.status == E_INVARIANT
+
+
+@pytest.mark.parametrize("dtype,B,G,V,tau", [(torch.bfloat16, 256, 8, 128256, 0.2),
+                                             (torch.float32, 160, 16, 151936, 0.3)])
+def test_early_exit_matches_oracle(verifier, oracle, dtype, B, G, V, tau):
+    """dsdv_verify_early_exit: rows past a sequence's first rejection are not
+    streamed, the round's results are the reference's."""
+    crit = Oracle.crit(2.0, 0.2, 0.5, 10)
+    draft, target, tokens = _window(verifier, dtype, B, G, V, 44, 6, 2)
+    from paper_2511_11733_b200.dsdv import VerifyParams
+    p = VerifyParams(gamma=G, tau=tau, ratio_limit=2.0, gap_limit=0.2, overlap_floor=0.5,
+                     top_m=10, seed=6, window=2)
+    verifier.streamed_bytes(reset=True)
+    full = verifier.verify(draft, target, tokens, p, vocab=V)
+    verifier.sync(p, full, batch=B, vocab=V)
+    full_bytes = verifier.streamed_bytes(reset=True)
+    early = verifier.verify(draft, target, tokens, p, vocab=V, early_exit=True)
+    verifier.sync(p, early, batch=B, vocab=V)
+    early_bytes = verifier.streamed_bytes(reset=True)
+    g = early.to_host()
+    ref = oracle.verify_batch(host_logits(draft), host_logits(target), tokens.cpu().numpy(),
+                              [(tau, crit)], window_uniforms(6, 2, B, G), V,
+                              all_positions=False)[0]
+    rep = compare_batch(ref, g, all_positions=False)
+    _report(rep, f"early exit {dtype} B={B}")
+    assert rep.ok(), rep.mismatches[:10]
+    assert rep.eps_events <= 3
+    f = full.to_host()
+    for k in ("accepted_count", "extra_token", "extra_source", "key_count", "status"):
+        assert torch.equal(f[k], g[k]), k
+    print(f"[early exit] streamed {early_bytes / 1e9:.3f} GB vs {full_bytes / 1e9:.3f} GB full")
+    assert early_bytes < 0.8 * full_bytes
