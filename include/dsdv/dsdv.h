@@ -156,6 +156,26 @@ dsdv_status dsdv_verify_early_exit(dsdv_ctx *ctx, const dsdv_params *params,
                                    const int32_t *draft_tokens, const dsdv_outputs *out,
                                    void *stream);
 
+/* dsdv_window_stats with the overlap clause decided by the caller's NormMatch
+ * (norm_match_in[B][gamma], device), so any 1 <= top_m <= V works: the C++
+ * drop-in computes it with dsdv_norm_match_rows when top_m exceeds the fused
+ * kernel's warp selection (32). */
+dsdv_status dsdv_window_stats_nm(dsdv_ctx *ctx, const dsdv_params *params,
+                                 const void *draft_logits, const void *target_logits,
+                                 const int32_t *draft_tokens, const double *norm_match_in,
+                                 const dsdv_outputs *out, void *stream);
+
+/* NormMatch (norm_match, verifier.cpp:119-134) of gamma positions for any
+ * top_m: the top_m ids of each fp64 probability row by (p desc, id asc)
+ * (top_ids, :40-51: a stable segmented radix sort on the device), then
+ * |T cap D| / top_m per position. Rows are [gamma][row_stride]; scratch is
+ * device memory of dsdv_norm_match_scratch_bytes(). Asynchronous. */
+size_t dsdv_norm_match_scratch_bytes(int32_t gamma, int32_t vocab, int32_t row_stride);
+dsdv_status dsdv_norm_match_rows(dsdv_ctx *ctx, const double *draft_probs,
+                                 const double *target_probs, int32_t gamma, int32_t vocab,
+                                 int32_t row_stride, int32_t top_m, void *scratch,
+                                 size_t scratch_bytes, double *norm_match_out, void *stream);
+
 /* Logit bytes the fused verifier's producers copied from global memory since
  * the last reset (accumulated over launches on this context). Synchronous:
  * waits for the device. reset != 0 clears the counter after reading. */

@@ -13,6 +13,10 @@
 
 namespace dsdv {
 int fused_max_vocab(int esize, int top_m);
+size_t norm_match_scratch_bytes(int gamma, int V, int stride);
+cudaError_t launch_norm_match(const double *draft, const double *target, int gamma, int V,
+                              int stride, int M, void *scratch, double *nm_out,
+                              cudaStream_t stream);
 template <class In>
 cudaError_t launch_fused(const DevParams &, const void *, const void *, const int32_t *,
                          const DevOut &, const DevScratch &, cudaStream_t, int *);
@@ -202,7 +206,8 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
                       const void *target, const int32_t *tokens, const dsdv_outputs *out,
                       void *stream, bool stats_only, double *topv = nullptr,
                       int32_t *topi = nullptr, int npeer = 0,
-                      const long long *peer_delta = nullptr, bool early_exit = false) {
+                      const long long *peer_delta = nullptr, bool early_exit = false,
+                      const double *nm_in = nullptr) {
   const bool partial = topv != nullptr;
   if (!ctx) return DSDV_E_INVARIANT;
   DevParams d;
@@ -211,6 +216,7 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   d.stats_only = stats_only ? 1 : 0;
   d.partial = partial ? 1 : 0;
   d.early_exit = early_exit ? 1 : 0;
+  d.nm_in = nm_in;
   if (partial && !topi)
     return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_stats: top lists are required");
   if (!draft || !target || !tokens || !out)
@@ -405,6 +411,48 @@ dsdv_status dsdv_verify_early_exit(dsdv_ctx *ctx, const dsdv_params *params,
                                    void *stream) {
   return run_fused(ctx, params, draft_logits, target_logits, draft_tokens, out, stream, false,
                    nullptr, nullptr, 0, nullptr, true);
+}
+
+dsdv_status dsdv_window_stats_nm(dsdv_ctx *ctx, const dsdv_params *params,
+                                 const void *draft_logits, const void *target_logits,
+                                 const int32_t *draft_tokens, const double *norm_match_in,
+                                 const dsdv_outputs *out, void *stream) {
+  if (!ctx || !params) return DSDV_E_INVARIANT;
+  if (!norm_match_in)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_window_stats_nm: norm_match_in is required");
+  if (params->top_m < 1)
+    return fail(ctx, DSDV_E_INVARIANT, "criteria.top_m must be >= 1, got %d", params->top_m);
+  // the overlap clause comes from the caller; the kernel's own selection is
+  // reduced to one id per row (its NormMatch output is the caller's value)
+  dsdv_params q = *params;
+  q.top_m = 1;
+  return run_fused(ctx, &q, draft_logits, target_logits, draft_tokens, out, stream, true,
+                   nullptr, nullptr, 0, nullptr, false, norm_match_in);
+}
+
+size_t dsdv_norm_match_scratch_bytes(int32_t gamma, int32_t vocab, int32_t row_stride) {
+  return dsdv::norm_match_scratch_bytes(gamma, vocab, row_stride);
+}
+
+dsdv_status dsdv_norm_match_rows(dsdv_ctx *ctx, const double *draft_probs,
+                                 const double *target_probs, int32_t gamma, int32_t vocab,
+                                 int32_t row_stride, int32_t top_m, void *scratch,
+                                 size_t scratch_bytes, double *norm_match_out, void *stream) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  if (!draft_probs || !target_probs || !scratch || !norm_match_out || gamma < 1 || vocab < 1 ||
+      row_stride < vocab)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_norm_match_rows: bad argument");
+  if (top_m < 1 || top_m > vocab)
+    return fail(ctx, DSDV_E_INVARIANT, "top_m %d outside [1, %d]", top_m, vocab);
+  if (scratch_bytes < dsdv::norm_match_scratch_bytes(gamma, vocab, row_stride))
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_norm_match_rows: scratch too small");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  e = dsdv::launch_norm_match(draft_probs, target_probs, gamma, vocab, row_stride, top_m, scratch,
+                              norm_match_out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "norm_match launch");
+  ctx->launches += 1;
+  return DSDV_OK;
 }
 
 dsdv_status dsdv_streamed_bytes(dsdv_ctx *ctx, int reset, uint64_t *bytes) {

@@ -47,6 +47,7 @@ struct DevParams {
   int partial;      // 1: dsdv_shard_stats (partial records of a vocabulary slice only)
   int need_z;       // 0 < tau < 1
   int early_exit;   // 1: dsdv_verify_early_exit (rows past a sequence's first rejection are skipped)
+  const double *nm_in;  // dsdv_window_stats_nm: caller's NormMatch [B][gamma] (any top_m)
   float tau_f, omt_f;
   double tau, ratio_limit, gap_limit, overlap_floor, eps_u, eps_lambda;
   uint64_t seed, window;

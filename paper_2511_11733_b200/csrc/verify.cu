@@ -30,7 +30,10 @@
 // The extra draw (residual of a rejected position, :198-213, :245-246, or the
 // bonus draw, :253-256) is needed by a position whose predecessors are not
 // already known to have stopped the window. The epilogue posts it back to the
-// producer as a "sample item": the rows are streamed again (L2-resident) and
+// producer as a "sample item": the rows are streamed again (from HBM: after
+// 16+ stages of chip-wide streaming they are no longer in L2, see
+// scripts/micro/l2keep.cu; this re-read is the traffic above the algorithmic
+// bytes in profiles/) and
 // the compute warps turn them into per-tile sums of the residual / bonus
 // weights; the epilogue then scans the tile sums for u * W and resolves the
 // crossing tile (sample_with_uniform, distribution.cpp:103-114). The last item
@@ -94,8 +97,16 @@ struct Ring {
   static constexpr int kStages = sizeof(Acc) == 8 ? 4 : 5;
 #endif
 };
-constexpr int kMaxTiles = 1024;      // blocks per slot: (chunk, warp), kVecs*32*VEC ids each
-constexpr int kAreaBytes = 8 * kMaxTiles;  // per-slot block maxima (2 x int), or sample tiles (double)
+// Blocks per slot, (chunk, warp) of kVecs*32*VEC ids each: per-slot block
+// maxima (2 x int) or sample tiles (double). fp64 rows have 2048-id chunks,
+// so their slots carry more (the fp64 ring is one stage shorter): the fused
+// kernel takes V <= 64 * CH for bf16 / fp32 (524,288 / 262,144) and
+// V <= 116 * 2048 = 237,568 for fp64.
+template <class Acc>
+struct Area {
+  static constexpr int kTiles = sizeof(Acc) == 8 ? 1856 : 1024;
+  static constexpr int kBytes = 8 * kTiles;
+};
 constexpr int kCap = 256;            // captured top-m candidates per row and item
 // Sample-request queue. Bound: a request is outstanding from its posting until
 // the epilogue finishes its sample item. Stream items the producer issued but
@@ -181,7 +192,7 @@ struct Slot {
   // regular item: per-block max keys of l_t / l_d ([2][nblocks] ints, read only
   // by the capture-overflow fallback); sample item: per-tile weight sums
   // ([ntiles] doubles). See SlotView.
-  alignas(16) uint8_t area[kAreaBytes];
+  alignas(16) uint8_t area[Area<Acc>::kBytes];
 };
 
 // Typed views of a slot's area for one launch shape.
@@ -1116,7 +1127,7 @@ __device__ __noinline__ double exact_lse_mix_warp(const In *rt, const In *rd, in
 // :112-117, norm_match :119-134, is_key :136-159, effective distribution
 // :231-233 with soften's short-circuits :170-172).
 template <class In>
-__device__ __noinline__ void evaluate_position(const double (&mrg)[7], int diff, int shared,
+__device__ __noinline__ void evaluate_position(const double (&mrg)[7], int diff, double nm,
                                                const DevParams &p, const In *rt, const In *rd,
                                                int y, bool pair, PosEval &ev) {
   using Acc = typename InTraits<In>::Acc;
@@ -1162,7 +1173,7 @@ __device__ __noinline__ void evaluate_position(const double (&mrg)[7], int diff,
   const bool ratio = certain ? ratio_cert : ratio_rel;
   const double gap = fabs(ev.p_t_y - ev.p_d_y);
   const bool gapc = gap > p.gap_limit;
-  ev.nm = (double)shared / (double)p.top_m;
+  ev.nm = nm;  // a double shared / m, compared as the reference does (:133, :156)
   const bool overlap = ev.nm < p.overlap_floor;
   ev.key = (ratio || gapc || overlap) ? 1 : 0;
   // near-threshold bookkeeping (fp32 statistics vs the fp64 reference)
@@ -1590,7 +1601,11 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
       PosEval ev;
       if (lane == 0) {
         const int y = pair ? tokens[(size_t)b * p.gamma + j] : 0;
-        evaluate_position<In>(mrg, diff, shared, p, rt, rd, y, pair, ev);
+        // NormMatch of a top_m beyond the warp selection comes from the caller
+        // (dsdv_window_stats_nm); otherwise from the selected top lists
+        const double nm = (pair && p.nm_in) ? p.nm_in[(size_t)b * p.gamma + j]
+                                            : (double)shared / (double)p.top_m;
+        evaluate_position<In>(mrg, diff, nm, p, rt, rd, y, pair, ev);
       }
       const int need_exact = __shfl_sync(0xffffffffu, lane == 0 ? ev.need_exact : 0, 0);
       if (need_exact) {
@@ -1826,7 +1841,7 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
   int n = 0, next = -1;
   bool exhausted = false;
   for (;;) {
-    // sample requests first: their rows are still L2-resident
+    // sample requests first: the sequence's completion waits on them
     const int head = vload(&sm.req_head);
     if (head != vload(&sm.req_tail)) {
       const int r = head % kReq;
@@ -1997,7 +2012,7 @@ cudaError_t launch_fused(const DevParams &p, const void *draft, const void *targ
   DevParams q = p;
   q.n_chunks = (p.vocab_local + CH - 1) / CH;
   const int ntiles = q.n_chunks * fz::kCW;
-  if (ntiles > fz::kMaxTiles || 8 * q.n_chunks * fz::kCW > fz::kAreaBytes)
+  if (ntiles > fz::Area<typename InTraits<In>::Acc>::kTiles)
     return cudaErrorInvalidValue;
   return q.early_exit ? launch_fused_t<In, true>(q, draft, target, tokens, o, s, stream, grid_out)
                       : launch_fused_t<In, false>(q, draft, target, tokens, o, s, stream, grid_out);
@@ -2007,10 +2022,8 @@ cudaError_t launch_fused(const DevParams &p, const void *draft, const void *targ
 // sample tiles, must fit the slot area).
 int fused_max_vocab(int esize, int top_m) {
   (void)top_m;
-  const int by_tiles = fz::kMaxTiles / fz::kCW;
-  const int by_area = fz::kAreaBytes / (8 * fz::kCW);
-  const int chunks = by_tiles < by_area ? by_tiles : by_area;
-  return chunks * (fz::kRowBytes / esize);
+  const int tiles = esize == 8 ? fz::Area<double>::kTiles : fz::Area<float>::kTiles;
+  return tiles / fz::kCW * (fz::kRowBytes / esize);
 }
 
 template cudaError_t launch_fused<__nv_bfloat16>(const DevParams &, const void *, const void *,

@@ -180,6 +180,13 @@ struct DeviceWindow {
   double *d_records = nullptr;
   int32_t *d_position = nullptr, *d_token = nullptr, *d_status = nullptr;
   double *d_u = nullptr;
+  // top_m beyond the fused kernel's warp selection (32): NormMatch from an
+  // exact device sort of the probability rows (dsdv_norm_match_rows)
+  int m = 1;
+  bool big_m = false;
+  double *d_pd = nullptr, *d_pt = nullptr, *d_nm = nullptr;
+  void *d_scratch = nullptr;
+  size_t scratch_bytes = 0;
 
   DeviceWindow(Engine &e, const std::vector<const Distribution *> &draft,
                const std::vector<const Distribution *> &target, const std::vector<int> &tokens,
@@ -190,11 +197,17 @@ struct DeviceWindow {
     stride = (V + 1) & ~1;  // 16-byte rows of fp64
     const int G1 = gamma + 1;
     const size_t rows_draft = (size_t)gamma * stride, rows_target = (size_t)G1 * stride;
+    m = c.top_m < V ? c.top_m : V;  // verifier.cpp:155
+    big_m = m > 32;
+    if (big_m) scratch_bytes = dsdv_norm_match_scratch_bytes(gamma, V, stride);
     const size_t bytes = carve_size<double>(rows_draft) + carve_size<double>(rows_target) +
                          carve_size<int32_t>(gamma) + 6 * carve_size<int32_t>(1) +
                          2 * carve_size<uint8_t>(gamma) + 8 * carve_size<double>(gamma) +
                          carve_size<double>((size_t)G1 * kRecWords) + 3 * carve_size<int32_t>(1) +
-                         carve_size<double>(1) + carve_size<uint8_t>(1);
+                         carve_size<double>(1) + carve_size<uint8_t>(1) +
+                         (big_m ? 2 * carve_size<double>(rows_draft) + carve_size<double>(gamma) +
+                                      carve_size<char>(scratch_bytes)
+                                : 0);
     Carve dv(eng.dev_arena(bytes));
     d_draft = dv.take<double>(rows_draft);
     d_target = dv.take<double>(rows_target);
@@ -221,13 +234,32 @@ struct DeviceWindow {
     d_token = dv.take<int32_t>(1);
     d_status = dv.take<int32_t>(1);
     d_u = dv.take<double>(1);
+    if (big_m) {
+      d_pd = dv.take<double>(rows_draft);
+      d_pt = dv.take<double>(rows_draft);
+      d_nm = dv.take<double>(gamma);
+      d_scratch = dv.take<char>(scratch_bytes);
+    }
 
     // stage the rows in pinned memory, one copy
-    const size_t hbytes = (rows_draft + rows_target) * sizeof(double) + gamma * sizeof(int32_t);
+    const size_t hbytes = (rows_draft + rows_target + (big_m ? 2 * rows_draft : 0)) *
+                              sizeof(double) +
+                          gamma * sizeof(int32_t);
     char *h = static_cast<char *>(eng.host_arena(hbytes));
     double *hd = reinterpret_cast<double *>(h);
     double *ht = hd + rows_draft;
-    int32_t *htok = reinterpret_cast<int32_t *>(ht + rows_target);
+    double *hpd = ht + rows_target, *hpt = hpd + (big_m ? rows_draft : 0);
+    int32_t *htok = reinterpret_cast<int32_t *>(hpt + (big_m ? rows_draft : 0));
+    if (big_m) {
+      // probability rows as given (top_ids orders by p, verifier.cpp:40-51)
+      for (int j = 0; j < gamma; ++j) {
+        std::memcpy(hpd + (size_t)j * stride, draft[j]->probs().data(), V * sizeof(double));
+        std::memcpy(hpt + (size_t)j * stride, target[j]->probs().data(), V * sizeof(double));
+        for (int i = V; i < stride; ++i) hpd[(size_t)j * stride + i] = hpt[(size_t)j * stride + i] = 0.0;
+      }
+      cudaMemcpyAsync(d_pd, hpd, rows_draft * sizeof(double), cudaMemcpyHostToDevice, eng.stream);
+      cudaMemcpyAsync(d_pt, hpt, rows_draft * sizeof(double), cudaMemcpyHostToDevice, eng.stream);
+    }
     for (int j = 0; j < gamma; ++j) put_log_row(hd + (size_t)j * stride, *draft[j], stride);
     for (int j = 0; j < G1; ++j) put_log_row(ht + (size_t)j * stride, *target[j], stride);
     for (int j = 0; j < gamma; ++j) htok[j] = tokens[j];
@@ -243,7 +275,7 @@ struct DeviceWindow {
     prm.vocab = V;
     prm.row_stride = stride;
     prm.dtype = DSDV_DTYPE_F64;
-    prm.top_m = c.top_m;
+    prm.top_m = big_m ? 1 : c.top_m;  // big_m: the overlap clause comes from d_nm
     prm.tau = tau;
     prm.ratio_limit = c.ratio_limit;
     prm.gap_limit = c.gap_limit;
@@ -258,7 +290,14 @@ struct DeviceWindow {
   }
 
   WindowStats stats() {
-    eng.check(dsdv_window_stats(eng.ctx, &prm, d_draft, d_target, d_tokens, &out, eng.stream));
+    if (big_m) {
+      eng.check(dsdv_norm_match_rows(eng.ctx, d_pd, d_pt, gamma, V, stride, m, d_scratch,
+                                     scratch_bytes, d_nm, eng.stream));
+      eng.check(dsdv_window_stats_nm(eng.ctx, &prm, d_draft, d_target, d_tokens, d_nm, &out,
+                                     eng.stream));
+    } else {
+      eng.check(dsdv_window_stats(eng.ctx, &prm, d_draft, d_target, d_tokens, &out, eng.stream));
+    }
     WindowStats ws;
     ws.gamma = gamma;
     ws.key.resize(gamma);

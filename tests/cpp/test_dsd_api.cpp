@@ -8,6 +8,12 @@
 //                           prints the accepted count of every round of
 //                           generate() on the default divergent pair
 //                           (compared with oracle/_ref by tests/test_cpp_api.py)
+//   test_dsd_api rows FILE  one (draft, target) probability-row pair at any
+//                           vocabulary and top_m: prints norm_match, is_key and
+//                           the accepted counts of generate() with categorical
+//                           models, then the mean ms per round
+//                           (tests/test_cpp_api.py, scripts/dropin_timing.py)
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -275,6 +281,37 @@ int main(int argc, char **argv) {
                                           std::atoi(argv[5]), vp, rng);
       for (const VerificationResult &r : g.rounds) std::printf("%d ", r.accepted_count);
       std::printf("\n");
+      return 0;
+    }
+    if (mode == "rows" && argc == 3) {
+      FILE *f = std::fopen(argv[2], "rb");
+      if (!f) return 3;
+      int32_t V, gamma, top_m, max_new, y;
+      double tau, ratio, gap, overlap;
+      uint64_t seed;
+      bool ok = std::fread(&V, 4, 1, f) == 1 && std::fread(&gamma, 4, 1, f) == 1 &&
+                std::fread(&tau, 8, 1, f) == 1 && std::fread(&ratio, 8, 1, f) == 1 &&
+                std::fread(&gap, 8, 1, f) == 1 && std::fread(&overlap, 8, 1, f) == 1 &&
+                std::fread(&top_m, 4, 1, f) == 1 && std::fread(&seed, 8, 1, f) == 1 &&
+                std::fread(&max_new, 4, 1, f) == 1 && std::fread(&y, 4, 1, f) == 1;
+      std::vector<double> pd(V), pt(V);
+      ok = ok && std::fread(pd.data(), 8, V, f) == (size_t)V &&
+           std::fread(pt.data(), 8, V, f) == (size_t)V;
+      std::fclose(f);
+      if (!ok) return 3;
+      const Distribution dd(pd), dt(pt);
+      const KeyCriteria c{ratio, gap, overlap, top_m};
+      std::printf("%.17g\n", norm_match(dt, dd, std::min<int>(top_m, V)));
+      std::printf("%d\n", is_key(dt, dd, y, c) ? 1 : 0);
+      SeededStream rng(seed);
+      const VerifyParams vp{gamma, tau, c};
+      const auto t0 = std::chrono::steady_clock::now();
+      const GenerationResult g = generate(TokenModel::categorical(dd), TokenModel::categorical(dt),
+                                          Context{}, max_new, vp, rng);
+      const auto t1 = std::chrono::steady_clock::now();
+      for (const VerificationResult &r : g.rounds) std::printf("%d ", r.accepted_count);
+      std::printf("\n%.6f\n",
+                  std::chrono::duration<double, std::milli>(t1 - t0).count() / g.rounds.size());
       return 0;
     }
     kat_primitives();

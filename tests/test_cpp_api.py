@@ -92,3 +92,50 @@ def test_rest_of_reference_builds_against_the_drop_in():
                "-L/usr/local/cuda/lib64", "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
+
+
+def write_rows_case(path, pd, pt, gamma, tau, crit, seed, max_new, y):
+    import struct
+    import numpy as np
+    V = pd.size
+    with open(path, "wb") as f:
+        f.write(struct.pack("<iiddddiQii", V, gamma, tau, crit[0], crit[1], crit[2], crit[3],
+                            seed, max_new, y))
+        f.write(np.ascontiguousarray(pd, dtype=np.float64).tobytes())
+        f.write(np.ascontiguousarray(pt, dtype=np.float64).tobytes())
+
+
+def rows_pair(V, seed):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    lt = rng.normal(size=V) * 3.0
+    ld = lt + rng.normal(size=V) * 1.0
+    pt = np.exp(lt - lt.max())
+    pd = np.exp(ld - ld.max())
+    # Distribution::from_weights-style normalisation (distribution.cpp:54-63)
+    return pd / pd.sum(), pt / pt.sum()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("V,top_m", [(151936, 10), (151936, 64), (5000, 200)])
+def test_dropin_any_vocab_and_top_m_against_reference(ref_oracle, tmp_path, V, top_m):
+    """The drop-in beyond the fused kernel's former limits: Qwen2's V=151936
+    (fp64 rows) and top_m > 32 (exact device sort for NormMatch), against the
+    reference's own norm_match / is_key / generate (oracle/_ref)."""
+    import numpy as np
+    pd, pt = rows_pair(V, 7 + top_m)
+    y = int(np.argsort(-pd)[3])
+    crit = (2.0, 0.2, 0.5, top_m)
+    f = tmp_path / "rows.bin"
+    write_rows_case(f, pd, pt, 4, 0.2, crit, 11, 12, y)
+    r = subprocess.run([str(EXE), "rows", str(f)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = r.stdout.split("\n")
+    nm, key, ks = float(lines[0]), int(lines[1]), [int(x) for x in lines[2].split()]
+    st, ref_nm = ref_oracle.norm_match(pt, pd, min(top_m, V))
+    assert st == 0 and nm == ref_nm
+    st, ref_key = ref_oracle.is_key(pt, pd, y, *crit)
+    assert st == 0 and bool(key) == ref_key
+    from oracle.oracle_lib import Oracle
+    ref_ks = ref_oracle.generate_iid(pd, pt, 4, 0.2, Oracle.crit(*crit), 12, 11)
+    assert ks == ref_ks
