@@ -176,6 +176,34 @@ dsdv_status dsdv_norm_match_rows(dsdv_ctx *ctx, const double *draft_probs,
                                  int32_t row_stride, int32_t top_m, void *scratch,
                                  size_t scratch_bytes, double *norm_match_out, void *stream);
 
+/* ---- threshold calibration (calibrate.cpp:51-148) ------------------------ */
+typedef struct {
+  double ratio_limit, gap_limit, overlap_floor; /* KeyCriteria (verifier.hpp:32-43) */
+  int32_t top_m;
+} dsdv_key_criteria;
+
+typedef struct {
+  int32_t vocab;       /* 2 <= V <= 8 (EnumerationGuard, enumerate.hpp:31) */
+  int32_t horizon;     /* 1..4 */
+  int64_t rows_offset; /* into the rows array: (V + 1) draft rows, then (V + 1) target rows of
+                          V doubles; row s < V follows last token s, row V the prompt */
+} dsdv_calib_item;
+
+typedef struct {
+  double avg_accepted_len; /* mean over items of E[accepted] + 1 */
+  double divergence;       /* mean TV(adaptive, strict tau = 0) over the horizon */
+  int32_t feasible;        /* divergence <= budget */
+  int32_t status;          /* DSDV_OK, or the error an item's enumeration would raise */
+} dsdv_grid_eval;
+
+/* evaluate_point (calibrate.cpp:51-76) for every grid point, on the device: one
+ * thread per (point, item) runs the exact enumerations in fp64 with the
+ * reference's operation order. Host arrays in and out; synchronous. */
+dsdv_status dsdv_calibrate(dsdv_ctx *ctx, const dsdv_calib_item *items, int32_t n_items,
+                           const double *rows, int64_t n_row_doubles,
+                           const dsdv_key_criteria *points, int32_t n_points, double tau,
+                           int32_t gamma, double budget, dsdv_grid_eval *out);
+
 /* Logit bytes the fused verifier's producers copied from global memory since
  * the last reset (accumulated over launches on this context). Synchronous:
  * waits for the device. reset != 0 clears the counter after reading. */

@@ -336,6 +336,7 @@ class RefOracle:
         L.ref_verify_batch_f32.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _fp, _fp, _ip,
                                            C.c_double, C.c_double, C.c_double, C.c_double,
                                            C.c_int, _dp, C.c_int, _ip, _ip, _ip]
+        L.ref_calibrate_c8.argtypes = [C.c_double, _dp, _dp, C.c_int]
         L.ref_generate_iid.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_double, C.c_int, C.c_int, C.c_uint64, _ip,
                                        C.c_int]
@@ -435,6 +436,16 @@ class RefOracle:
                                     crit.gap_limit, crit.overlap_floor, crit.top_m,
                                     self._a(uniforms), nthreads or os.cpu_count(), k, e, s)
         return k, e, s
+
+    def calibrate_c8(self, budget):
+        """Acceptance criterion 8 through the reference's calibrate_thresholds:
+        (winner [len, divergence, ratio, gap, overlap], grid log [n][6])."""
+        best = np.zeros(5)
+        log = np.zeros((64, 6))
+        n = self.L.ref_calibrate_c8(budget, best, log, 64)
+        if n < 0:
+            raise RuntimeError("ref_calibrate_c8 failed")
+        return best, log[:n]
 
     def temperature_scale(self, p, T):
         p = self._a(p)

@@ -25,6 +25,7 @@
 #include "dsd/error.hpp"
 #include "dsd/rng.hpp"
 #include "dsd/token_model.hpp"
+#include "dsd/calibrate.hpp"
 #include "dsd/verifier.hpp"
 #include "../include/dsdv/philox.h"
 
@@ -339,6 +340,58 @@ int ref_enumerate_first(const double *pd, const double *pt, int V, int gamma, do
     return 0;
   } catch (...) {
     return -code_of(std::current_exception());
+  }
+}
+
+// acceptance criterion 8 (acceptance.cpp:345-398) through the reference's own
+// calibrate_thresholds: the winner (len, divergence, ratio, gap, overlap) and the
+// grid log [64][6] (ratio, gap, overlap, len, divergence, feasible)
+int ref_calibrate_c8(double budget, double *best, double *log, int cap) {
+  try {
+    using namespace dsd;
+    const std::vector<ValidationItem> items = {
+        ValidationItem{Context{}, TokenModel::categorical(Distribution({0.5, 0.5})),
+                       TokenModel::categorical(Distribution({0.9, 0.1})), 2},
+        ValidationItem{Context{},
+                       TokenModel::categorical(Distribution({0.15, 0.2, 0.25, 0.2, 0.1, 0.1})),
+                       TokenModel::categorical(Distribution({0.45, 0.3, 0.1, 0.08, 0.04, 0.03})),
+                       2},
+        ValidationItem{Context({0}),
+                       TokenModel::markov({Distribution({0.6, 0.2, 0.2}),
+                                           Distribution({0.25, 0.5, 0.25}),
+                                           Distribution({0.2, 0.3, 0.5})},
+                                          Distribution({0.4, 0.3, 0.3})),
+                       TokenModel::markov({Distribution({0.8, 0.1, 0.1}),
+                                           Distribution({0.1, 0.8, 0.1}),
+                                           Distribution({0.05, 0.15, 0.8})},
+                                          Distribution({0.5, 0.3, 0.2})),
+                       2},
+        ValidationItem{Context{}, TokenModel::categorical(Distribution({0.3, 0.3, 0.2, 0.2})),
+                       TokenModel::categorical(Distribution({0.55, 0.25, 0.15, 0.05})), 2},
+        ValidationItem{Context{}, TokenModel::categorical(Distribution({0.6, 0.25, 0.15})),
+                       TokenModel::categorical(Distribution({0.6, 0.25, 0.15})), 2},
+    };
+    const CalibrationResult r =
+        calibrate_thresholds(items, 0.5, budget, ThresholdGrid::defaults(), 3, 6);
+    best[0] = r.avg_accepted_len;
+    best[1] = r.divergence;
+    best[2] = r.criteria.ratio_limit;
+    best[3] = r.criteria.gap_limit;
+    best[4] = r.criteria.overlap_floor;
+    int n = 0;
+    for (const GridPointEval &e : r.grid_log) {
+      if (n >= cap) break;
+      double *row = log + 6 * n++;
+      row[0] = e.criteria.ratio_limit;
+      row[1] = e.criteria.gap_limit;
+      row[2] = e.criteria.overlap_floor;
+      row[3] = e.avg_accepted_len;
+      row[4] = e.divergence;
+      row[5] = e.feasible ? 1.0 : 0.0;
+    }
+    return n;
+  } catch (...) {
+    return -1;
   }
 }
 

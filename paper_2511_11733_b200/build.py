@@ -30,8 +30,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
               f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
 
-CU_SOURCES = ["verify.cu", "rows.cu", "shard.cu", "topm.cu", "abi.cu"]
-HOST_SOURCES = ["dsd_api.cpp"]
+CU_SOURCES = ["verify.cu", "rows.cu", "shard.cu", "topm.cu", "calib.cu", "abi.cu"]
+HOST_SOURCES = ["dsd_api.cpp", "calib_api.cpp"]
 
 
 def _run(cmd: list[str]) -> None:

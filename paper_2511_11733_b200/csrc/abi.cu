@@ -14,6 +14,12 @@
 namespace dsdv {
 int fused_max_vocab(int esize, int top_m);
 size_t norm_match_scratch_bytes(int gamma, int V, int stride);
+size_t calib_scratch_doubles(int max_vocab, int max_horizon, int gamma);
+cudaError_t launch_calibrate(const dsdv_calib_item *items, int n_items, const double *rows,
+                             const dsdv_key_criteria *points, int n_points, double tau, int gamma,
+                             double budget, double *scratch, size_t scratch_per_thread,
+                             double *len, double *tv, int32_t *status, dsdv_grid_eval *out,
+                             cudaStream_t stream);
 cudaError_t launch_norm_match(const double *draft, const double *target, int gamma, int V,
                               int stride, int M, void *scratch, double *nm_out,
                               cudaStream_t stream);
@@ -452,6 +458,65 @@ dsdv_status dsdv_norm_match_rows(dsdv_ctx *ctx, const double *draft_probs,
                               norm_match_out, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "norm_match launch");
   ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_calibrate(dsdv_ctx *ctx, const dsdv_calib_item *items, int32_t n_items,
+                           const double *rows, int64_t n_row_doubles,
+                           const dsdv_key_criteria *points, int32_t n_points, double tau,
+                           int32_t gamma, double budget, dsdv_grid_eval *out) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  if (!items || n_items < 1 || !rows || !points || n_points < 1 || !out)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_calibrate: bad argument");
+  if (gamma < 1 || gamma > 4)
+    return fail(ctx, DSDV_E_UNSUPPORTED, "enumeration guard exceeded: need gamma <= 4");
+  int maxV = 2, maxH = 1;
+  for (int i = 0; i < n_items; ++i) {
+    const dsdv_calib_item &it = items[i];
+    if (it.vocab < 2 || it.vocab > 8 || it.horizon < 1 || it.horizon > 4)
+      return fail(ctx, DSDV_E_UNSUPPORTED,
+                  "enumeration guard exceeded: need vocab <= 8, 1 <= horizon <= 4");
+    if (it.rows_offset < 0 ||
+        it.rows_offset + (int64_t)2 * (it.vocab + 1) * it.vocab > n_row_doubles)
+      return fail(ctx, DSDV_E_INVARIANT, "dsdv_calibrate: item %d rows out of range", i);
+    maxV = it.vocab > maxV ? it.vocab : maxV;
+    maxH = it.horizon > maxH ? it.horizon : maxH;
+  }
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  const size_t per = dsdv::calib_scratch_doubles(maxV, maxH, gamma);
+  const size_t nt = (size_t)n_points * n_items;
+  const size_t bytes = n_items * sizeof(dsdv_calib_item) + n_row_doubles * sizeof(double) +
+                       n_points * sizeof(dsdv_key_criteria) + nt * per * sizeof(double) +
+                       2 * nt * sizeof(double) + nt * sizeof(int32_t) +
+                       n_points * sizeof(dsdv_grid_eval) + 8 * 256;
+  char *d = nullptr;
+  e = cudaMalloc(&d, bytes);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(calibrate)");
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    char *p = d + off;
+    off = (off + n + 255) & ~size_t(255);
+    return p;
+  };
+  auto *d_items = reinterpret_cast<dsdv_calib_item *>(take(n_items * sizeof(dsdv_calib_item)));
+  auto *d_rows = reinterpret_cast<double *>(take(n_row_doubles * sizeof(double)));
+  auto *d_points = reinterpret_cast<dsdv_key_criteria *>(take(n_points * sizeof(dsdv_key_criteria)));
+  auto *d_scratch = reinterpret_cast<double *>(take(nt * per * sizeof(double)));
+  auto *d_len = reinterpret_cast<double *>(take(nt * sizeof(double)));
+  auto *d_tv = reinterpret_cast<double *>(take(nt * sizeof(double)));
+  auto *d_st = reinterpret_cast<int32_t *>(take(nt * sizeof(int32_t)));
+  auto *d_out = reinterpret_cast<dsdv_grid_eval *>(take(n_points * sizeof(dsdv_grid_eval)));
+  cudaMemcpy(d_items, items, n_items * sizeof(dsdv_calib_item), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_rows, rows, n_row_doubles * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_points, points, n_points * sizeof(dsdv_key_criteria), cudaMemcpyHostToDevice);
+  e = dsdv::launch_calibrate(d_items, n_items, d_rows, d_points, n_points, tau, gamma, budget,
+                             d_scratch, per, d_len, d_tv, d_st, d_out, nullptr);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(out, d_out, n_points * sizeof(dsdv_grid_eval), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "calibrate");
+  ctx->launches += 2;
   return DSDV_OK;
 }
 

@@ -699,6 +699,7 @@ void set_device(int device) {
   eng.ready();
 }
 unsigned long long launch_count() { return dsdv_launch_count(engine().ctx); }
+dsdv_ctx *context() { return engine().ctx; }
 }  // namespace gpu
 
 }  // namespace dsd

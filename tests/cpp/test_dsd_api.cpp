@@ -8,6 +8,8 @@
 //                           prints the accepted count of every round of
 //                           generate() on the default divergent pair
 //                           (compared with oracle/_ref by tests/test_cpp_api.py)
+//   test_dsd_api calib B   acceptance criterion 8's calibration (acceptance.cpp:345-398)
+//                           at budget B on the device: the winner, then the grid log
 //   test_dsd_api rows FILE  one (draft, target) probability-row pair at any
 //                           vocabulary and top_m: prints norm_match, is_key and
 //                           the accepted counts of generate() with categorical
@@ -22,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "dsd/calibrate.hpp"
 #include "dsd/error.hpp"
 #include "dsd/verifier.hpp"
 
@@ -283,6 +286,37 @@ int main(int argc, char **argv) {
       std::printf("\n");
       return 0;
     }
+    if (mode == "calib" && argc == 3) {
+      // the 5-item set of acceptance.cpp:346-368
+      const std::vector<ValidationItem> items = {
+          ValidationItem{Context{}, TokenModel::categorical(Distribution({0.5, 0.5})),
+                         TokenModel::categorical(Distribution({0.9, 0.1})), 2},
+          ValidationItem{Context{}, divergent_draft(), divergent_target(), 2},
+          ValidationItem{Context({0}),
+                         TokenModel::markov({Distribution({0.6, 0.2, 0.2}),
+                                             Distribution({0.25, 0.5, 0.25}),
+                                             Distribution({0.2, 0.3, 0.5})},
+                                            Distribution({0.4, 0.3, 0.3})),
+                         TokenModel::markov({Distribution({0.8, 0.1, 0.1}),
+                                             Distribution({0.1, 0.8, 0.1}),
+                                             Distribution({0.05, 0.15, 0.8})},
+                                            Distribution({0.5, 0.3, 0.2})),
+                         2},
+          ValidationItem{Context{}, TokenModel::categorical(Distribution({0.3, 0.3, 0.2, 0.2})),
+                         TokenModel::categorical(Distribution({0.55, 0.25, 0.15, 0.05})), 2},
+          ValidationItem{Context{}, TokenModel::categorical(Distribution({0.6, 0.25, 0.15})),
+                         TokenModel::categorical(Distribution({0.6, 0.25, 0.15})), 2},
+      };
+      const CalibrationResult r =
+          calibrate_thresholds(items, 0.5, std::atof(argv[2]), ThresholdGrid::defaults(), 3, 6);
+      std::printf("%.17g %.17g %.17g %.17g %.17g\n", r.avg_accepted_len, r.divergence,
+                  r.criteria.ratio_limit, r.criteria.gap_limit, r.criteria.overlap_floor);
+      for (const GridPointEval &e : r.grid_log)
+        std::printf("%.17g %.17g %.17g %.17g %.17g %d\n", e.criteria.ratio_limit,
+                    e.criteria.gap_limit, e.criteria.overlap_floor, e.avg_accepted_len,
+                    e.divergence, e.feasible ? 1 : 0);
+      return 0;
+    }
     if (mode == "rows" && argc == 3) {
       FILE *f = std::fopen(argv[2], "rb");
       if (!f) return 3;
@@ -303,8 +337,13 @@ int main(int argc, char **argv) {
       const KeyCriteria c{ratio, gap, overlap, top_m};
       std::printf("%.17g\n", norm_match(dt, dd, std::min<int>(top_m, V)));
       std::printf("%d\n", is_key(dt, dd, y, c) ? 1 : 0);
-      SeededStream rng(seed);
       const VerifyParams vp{gamma, tau, c};
+      {  // warm-up: device context, arenas, pinned staging
+        SeededStream warm(seed + 1);
+        (void)generate(TokenModel::categorical(dd), TokenModel::categorical(dt), Context{}, 1, vp,
+                       warm);
+      }
+      SeededStream rng(seed);
       const auto t0 = std::chrono::steady_clock::now();
       const GenerationResult g = generate(TokenModel::categorical(dd), TokenModel::categorical(dt),
                                           Context{}, max_new, vp, rng);

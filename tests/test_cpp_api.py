@@ -24,7 +24,8 @@ API = ["dsd::verify_round(", "dsd::generate(", "dsd::draft_window(", "dsd::is_ke
        "dsd::token_cross_entropy(", "dsd::sample_with_uniform(", "dsd::next_distribution(",
        "dsd::Distribution::from_weights(", "dsd::KeyCriteria::validate()",
        "dsd::VerifyParams::validate()", "dsd::TokenModel::categorical(",
-       "dsd::TokenModel::markov(", "dsd::temperature_scale(", "dsd::total_variation("]
+       "dsd::TokenModel::markov(", "dsd::temperature_scale(", "dsd::total_variation(",
+       "dsd::calibrate_thresholds(", "dsd::ThresholdGrid::defaults()"]
 
 
 def test_library_exports_the_reference_api():
@@ -139,3 +140,28 @@ def test_dropin_any_vocab_and_top_m_against_reference(ref_oracle, tmp_path, V, t
     from oracle.oracle_lib import Oracle
     ref_ks = ref_oracle.generate_iid(pd, pt, 4, 0.2, Oracle.crit(*crit), 12, 11)
     assert ks == ref_ks
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("budget,golden", [(0.05, "2.82772"), (0.2, "3.25921")])
+def test_calibration_on_device_reproduces_criterion8(ref_oracle, budget, golden):
+    """calibrate_thresholds with every grid point evaluated on the device
+    (dsdv_calibrate) against the reference's own calibrate_thresholds on
+    acceptance criterion 8's item set: the same winner, the same 64-point grid
+    log, and test_output.txt:52's lengths (len 2.82772 @ 0.05 -> 3.25921 @ 0.2)."""
+    r = subprocess.run([str(EXE), "calib", repr(budget)], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = [[float(x) for x in line.split()] for line in r.stdout.strip().splitlines()]
+    best, log = rows[0], rows[1:]
+    ref_best, ref_log = ref_oracle.calibrate_c8(budget)
+    assert f"{best[0]:g}" == golden
+    assert best[2:] == list(ref_best[2:])  # the same thresholds win
+    assert math.isclose(best[0], ref_best[0], rel_tol=1e-12)
+    assert math.isclose(best[1], ref_best[1], rel_tol=1e-12, abs_tol=1e-15)
+    assert len(log) == len(ref_log) == 64
+    for g, rr in zip(log, ref_log):
+        assert g[:3] == list(rr[:3])
+        assert math.isclose(g[3], rr[3], rel_tol=1e-12)
+        assert math.isclose(g[4], rr[4], rel_tol=1e-12, abs_tol=1e-15)
+        assert g[5] == rr[5]
