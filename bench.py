@@ -49,6 +49,7 @@ sys.path.insert(0, str(ROOT))
 B, GAMMA, V = 256, 8, 128256
 TAU, RATIO, GAP, OVERLAP, TOP_M = 0.2, 2.0, 0.2, 0.5, 10
 LOGITS_SEED = 42
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 METRIC = "verified draft tokens/s & % HBM roofline (V=128k, γ=8, B=256) at 1/2/4/8 GPU"
 UNIT = "verified draft tokens/s"
 
@@ -479,6 +480,11 @@ def run_sharded(args, rank, world, local_rank):
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
     alg_bytes = Bt * (2 * GAMMA + 1) * n * 2  # this rank's slice of every row
+    # peer stores per window (exchange="peer"): records [B][G+1][8] f64 + top lists
+    # [B][G][2][M] (f64 value, i32 id) + [B] masses f64 + [B] tokens i32, into
+    # each of the other ranks' buffers
+    M = min(TOP_M, V)
+    nvl_bytes = (world - 1) * (Bt * (GAMMA + 1) * 8 * 8 + Bt * GAMMA * 2 * M * 12 + Bt * 12)
     line = {
         "metric": METRIC, "value": Bt * GAMMA / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
@@ -501,11 +507,17 @@ def run_sharded(args, rank, world, local_rank):
                    "mean_accepted_k": mean_k, "status_errors": bad,
                    "host_enqueue_ms_per_step": host_ms,
                    "committed_tokens_per_s": committed / (ms_max * 1e-3)},
-        "roofline": {"bound": "hbm", "achieved": alg_bytes / (ms_max * 1e-3) / 1e9, "peak": hbm,
-                     "unit": "GB/s", "frac": alg_bytes / (ms_max * 1e-3) / 1e9 / hbm,
+        "roofline": {"bound": "hbm+nvlink", "achieved": alg_bytes / (ms_max * 1e-3) / 1e9,
+                     "peak": hbm, "unit": "GB/s",
+                     "frac": (alg_bytes / (hbm * 1e9) + nvl_bytes / (NVLINK_GBS * 1e9)) /
+                             (ms_max * 1e-3),
                      "traffic": None, "algorithmic_bytes_per_launch": alg_bytes,
-                     "note": "per-rank bytes over the whole sharded window (stats kernel + "
-                             "collectives + merge + extra draw)",
+                     "nvlink_bytes_out_per_window": nvl_bytes, "nvlink_peak_gbs": NVLINK_GBS,
+                     "roofline_us": (alg_bytes / (hbm * 1e9) + nvl_bytes / (NVLINK_GBS * 1e9)) * 1e6,
+                     "note": "frac = (this rank's logit bytes / HBM peak + the bytes it stores "
+                             "into its peers' exchange buffers / NVLink peer bandwidth) / window "
+                             "time; NVLink peak: the measured peer copy of B200_PROFILING.md "
+                             "(770 GB/s per direction)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback"},
         "e2e": {"value": Bt * GAMMA / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},

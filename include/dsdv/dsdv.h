@@ -176,6 +176,42 @@ dsdv_status dsdv_norm_match_rows(dsdv_ctx *ctx, const double *draft_probs,
                                  int32_t row_stride, int32_t top_m, void *scratch,
                                  size_t scratch_bytes, double *norm_match_out, void *stream);
 
+/* One whole vocabulary-sharded window on this rank in one call, with no
+ * collective: the exchange of dsdv_shard_stats_peers (records stored into every
+ * rank's buffer as items complete), the merge and its slice masses, RESOLVE and
+ * the tokens maximum, each followed by a flag round (dsdv_peer_signal /
+ * dsdv_peer_wait), then the peer-wait status folded into out->status (a timed-out
+ * round fails every sequence with DSDV_E_NCCL). buffer_bases[q] is rank q's
+ * exchange buffer (CUDA-IPC mapped): two sets of [nranks][rank_stride_bytes]
+ * (set = window_epoch & 1) followed by nranks uint64 arrival flags; rank_stride
+ * >= dsdv_shard_exchange_bytes(), a multiple of 256. window_epoch >= 1 grows by
+ * one per window (flag values 3e, 3e+1, 3e+2). out needs records, status and
+ * extra_token. Asynchronous on stream. */
+uint64_t dsdv_shard_exchange_bytes(int32_t batch, int32_t gamma, int32_t top_m);
+dsdv_status dsdv_shard_verify_peers(dsdv_ctx *ctx, const dsdv_params *params,
+                                    const void *draft_logits, const void *target_logits,
+                                    const int32_t *draft_tokens, int32_t nranks, int32_t rank,
+                                    void *const *buffer_bases, uint64_t rank_stride_bytes,
+                                    uint64_t window_epoch, uint64_t timeout_ns,
+                                    const dsdv_outputs *out, void *stream);
+
+/* Pipeline-sharded decoding emulation (the reference's
+ * run_pipeline, netsim.cpp:110-172): N logical stages, stage s on rank s mod
+ * nranks. For each unit u (compute_ns[u]: t0 per token for standard decoding,
+ * k t0 per window for DSD) the owner of stage 0 spins the compute, every link
+ * s -> s+1 spins t1_ns and, across GPUs, stores the committed-token payload
+ * into the next rank's buffer over NVLink and releases a per-source counter
+ * the receiver waits on; the last stage returns the commit to stage 0. The
+ * whole loop is enqueued here, in C++, on `stream` (one call per run).
+ * buffer_bases as for dsdv_shard_verify_peers (set 0 slot q receives rank q's
+ * payload, the nranks uint64 flags count its messages); run_index >= 1 grows
+ * per call. status (device int32) gets DSDV_E_NCCL if a wait times out. */
+dsdv_status dsdv_pipeline_run(dsdv_ctx *ctx, int32_t n_stages, int32_t nranks, int32_t rank,
+                              void *const *buffer_bases, uint64_t rank_stride_bytes,
+                              const uint64_t *compute_ns, int32_t n_units, uint64_t t1_ns,
+                              uint64_t run_index, uint64_t timeout_ns, int32_t *status,
+                              void *stream);
+
 /* ---- threshold calibration (calibrate.cpp:51-148) ------------------------ */
 typedef struct {
   double ratio_limit, gap_limit, overlap_floor; /* KeyCriteria (verifier.hpp:32-43) */

@@ -57,6 +57,14 @@ cudaError_t launch_peer_signal(char *const *bases, int nranks, int rank, unsigne
                                unsigned long long epoch, cudaStream_t stream);
 cudaError_t launch_peer_wait(const unsigned long long *flags, int nranks, unsigned long long epoch,
                              unsigned long long timeout_ns, int *status, cudaStream_t stream);
+cudaError_t launch_status_fold(const int32_t *peer_status, int32_t *status, int batch,
+                               cudaStream_t stream);
+cudaError_t launch_hop_send(unsigned long long t1_ns, int32_t *dst_payload, const int32_t *payload,
+                            unsigned long long *dst_flag, unsigned long long value,
+                            cudaStream_t stream);
+cudaError_t launch_hop_recv(const unsigned long long *flag, unsigned long long value,
+                            unsigned long long timeout_ns, int *status, const int32_t *slot,
+                            int32_t *payload, cudaStream_t stream);
 cudaError_t launch_synth(int dtype, int B, int gamma, int V, int stride, uint64_t seed,
                          void *draft, void *target, cudaStream_t stream);
 }  // namespace dsdv
@@ -69,6 +77,9 @@ struct dsdv_ctx {
   int2 *slots = nullptr;          // [positions]
   unsigned int *done = nullptr;   // [sequences]
   unsigned long long *stop = nullptr;      // [sequences] early-exit stop keys
+  // dsdv_shard_verify_peers: extra-draw position, uniform, tile sums, peer status
+  void *shard_scratch = nullptr;
+  size_t shard_scratch_cap = 0;
   unsigned long long *streamed = nullptr;  // logit bytes copied by the fused kernel
   unsigned long long *trace = nullptr;  // DSDV_TRACE builds: [grid][kTraceWords]
   size_t flags_cap = 0;
@@ -325,6 +336,7 @@ dsdv_status dsdv_destroy(dsdv_ctx *ctx) {
   if (ctx->done) cudaFree(ctx->done);
   if (ctx->stop) cudaFree(ctx->stop);
   if (ctx->streamed) cudaFree(ctx->streamed);
+  if (ctx->shard_scratch) cudaFree(ctx->shard_scratch);
   if (ctx->trace) cudaFree(ctx->trace);
   delete ctx;
   return DSDV_OK;
@@ -872,6 +884,190 @@ dsdv_status dsdv_peer_tokens_max(dsdv_ctx *ctx, int32_t nranks, void *local_base
                                 (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "tokens max launch");
   ctx->launches += 1;
+  return DSDV_OK;
+}
+
+// Exchange layout of one rank's slot (paper_2511_11733_b200/sharded.py
+// ShardedVerifier.exchange_layout): packed records, top values, top ids, then
+// [B] slice masses and [B] RESOLVE tokens.
+static void exchange_layout(int B, int G, int M, uint64_t *o_rec, uint64_t *o_tv, uint64_t *o_ti,
+                            uint64_t *o_mass, uint64_t *o_tok, uint64_t *size) {
+  const uint64_t n_rec = (uint64_t)B * (G + 1) * DSDV_RECORD_WORDS * 8;
+  const uint64_t n_tv = (uint64_t)B * G * 2 * M * 8;
+  const uint64_t n_ti = (uint64_t)B * G * 2 * M * 4;
+  *o_rec = 0;
+  *o_tv = n_rec;
+  *o_ti = n_rec + n_tv;
+  const uint64_t packed = (n_rec + n_tv + n_ti + 7) / 8 * 8;
+  *o_mass = (packed + 7) / 8 * 8;
+  *o_tok = *o_mass + 8ull * B;
+  *size = *o_tok + 4ull * B;
+}
+
+uint64_t dsdv_shard_exchange_bytes(int32_t batch, int32_t gamma, int32_t top_m) {
+  uint64_t a, b, c, d, e, size;
+  exchange_layout(batch, gamma, top_m, &a, &b, &c, &d, &e, &size);
+  return size;
+}
+
+dsdv_status dsdv_shard_verify_peers(dsdv_ctx *ctx, const dsdv_params *params,
+                                    const void *draft_logits, const void *target_logits,
+                                    const int32_t *draft_tokens, int32_t nranks, int32_t rank,
+                                    void *const *buffer_bases, uint64_t rank_stride_bytes,
+                                    uint64_t window_epoch, uint64_t timeout_ns,
+                                    const dsdv_outputs *out, void *stream) {
+  if (!ctx || !params) return DSDV_E_INVARIANT;
+  if (nranks < 1 || nranks > DSDV_MAX_PEERS || rank < 0 || rank >= nranks || !buffer_bases ||
+      window_epoch < 1 || !out || !out->records || !out->status || !out->extra_token)
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_shard_verify_peers: bad argument");
+  const int B = params->batch, G = params->gamma;
+  const int M = params->top_m < params->vocab ? params->top_m : params->vocab;
+  uint64_t o_rec, o_tv, o_ti, o_mass, o_tok, size;
+  exchange_layout(B, G, M, &o_rec, &o_tv, &o_ti, &o_mass, &o_tok, &size);
+  if (rank_stride_bytes < size || rank_stride_bytes % 256)
+    return fail(ctx, DSDV_E_INVARIANT,
+                "dsdv_shard_verify_peers: rank stride %llu below the exchange size %llu",
+                (unsigned long long)rank_stride_bytes, (unsigned long long)size);
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  // scratch: position [B] i32, u [B] f64, tiles [B][TILE_WORDS] f64, peer status i32
+  const size_t need = 256 + (size_t)B * 4 + 256 + (size_t)B * 8 + 256 +
+                      (size_t)B * DSDV_SHARD_TILE_WORDS * 8 + 256 + 4;
+  if (need > ctx->shard_scratch_cap) {
+    if (ctx->shard_scratch) cudaFree(ctx->shard_scratch);
+    ctx->shard_scratch = nullptr;
+    e = cudaMalloc(&ctx->shard_scratch, need);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(shard scratch)");
+    ctx->shard_scratch_cap = need;
+  }
+  char *sp = (char *)ctx->shard_scratch;
+  auto take = [&](size_t n) {
+    char *q = sp;
+    sp += (n + 255) & ~size_t(255);
+    return q;
+  };
+  int32_t *position = (int32_t *)take((size_t)B * 4);
+  double *u = (double *)take((size_t)B * 8);
+  double *tiles = (double *)take((size_t)B * DSDV_SHARD_TILE_WORDS * 8);
+  int32_t *peer_status = (int32_t *)take(4);
+  e = cudaMemsetAsync(peer_status, 0, 4, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "peer status reset");
+  const uint64_t set_bytes = (uint64_t)nranks * rank_stride_bytes;
+  void *sets[DSDV_MAX_PEERS], *flags[DSDV_MAX_PEERS];
+  for (int q = 0; q < nranks; ++q) {
+    sets[q] = (char *)buffer_bases[q] + (window_epoch & 1) * set_bytes;
+    // dsdv_peer_signal / dsdv_peer_wait find the flags at nranks * stride past this
+    flags[q] = (char *)buffer_bases[q] + 2 * set_bytes - set_bytes;
+  }
+  const uint64_t f = 3 * window_epoch;
+  // 1. stats pass: the records land in every rank's set as items complete
+  dsdv_status st = dsdv_shard_stats_peers(ctx, params, draft_logits, target_logits, draft_tokens,
+                                          nranks, rank, sets, rank_stride_bytes, o_rec, o_tv,
+                                          o_ti, stream);
+  if (st == DSDV_OK) st = dsdv_peer_signal(ctx, nranks, rank, flags, rank_stride_bytes, f, stream);
+  if (st == DSDV_OK)
+    st = dsdv_peer_wait(ctx, nranks, flags[rank], rank_stride_bytes, f, timeout_ns, peer_status,
+                        stream);
+  // 2. merge (identical on every rank) + this slice's extra-draw masses
+  if (st == DSDV_OK)
+    st = dsdv_shard_merge_peers(ctx, params, nranks, rank, sets, rank_stride_bytes, o_rec, o_tv,
+                                o_ti, o_mass, draft_logits, target_logits, draft_tokens, out,
+                                position, u, tiles, stream);
+  if (st == DSDV_OK)
+    st = dsdv_peer_signal(ctx, nranks, rank, flags, rank_stride_bytes, f + 1, stream);
+  if (st == DSDV_OK)
+    st = dsdv_peer_wait(ctx, nranks, flags[rank], rank_stride_bytes, f + 1, timeout_ns,
+                        peer_status, stream);
+  // 3. the owning slice resolves the extra token; tokens max over the ranks
+  if (st == DSDV_OK)
+    st = dsdv_shard_resolve_peers(ctx, params, nranks, rank, sets, rank_stride_bytes, o_mass,
+                                  o_tok, draft_logits, target_logits, out->records, position, u,
+                                  out->status, tiles, stream);
+  if (st == DSDV_OK)
+    st = dsdv_peer_signal(ctx, nranks, rank, flags, rank_stride_bytes, f + 2, stream);
+  if (st == DSDV_OK)
+    st = dsdv_peer_wait(ctx, nranks, flags[rank], rank_stride_bytes, f + 2, timeout_ns,
+                        peer_status, stream);
+  if (st == DSDV_OK)
+    st = dsdv_peer_tokens_max(ctx, nranks, sets[rank], rank_stride_bytes, o_tok, B,
+                              out->extra_token, stream);
+  if (st != DSDV_OK) return st;
+  // a timed-out flag round fails every sequence of the window
+  e = dsdv::launch_status_fold(peer_status, out->status, B, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "status fold launch");
+  ctx->launches += 1;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_pipeline_run(dsdv_ctx *ctx, int32_t n_stages, int32_t nranks, int32_t rank,
+                              void *const *buffer_bases, uint64_t rank_stride_bytes,
+                              const uint64_t *compute_ns, int32_t n_units, uint64_t t1_ns,
+                              uint64_t run_index, uint64_t timeout_ns, int32_t *status,
+                              void *stream) {
+  if (!ctx || n_stages < 1 || nranks < 1 || nranks > DSDV_MAX_PEERS || rank < 0 ||
+      rank >= nranks || !compute_ns || n_units < 0 || run_index < 1 || run_index >= (1ull << 31) ||
+      (nranks > 1 && (!buffer_bases || rank_stride_bytes < 64 || rank_stride_bytes % 8)))
+    return fail(ctx, DSDV_E_INVARIANT, "dsdv_pipeline_run: bad argument");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  // this rank's own committed-token payload: slot `rank` of its set 0 (never a
+  // peer's destination)
+  int32_t *payload =
+      nranks > 1 ? (int32_t *)((char *)buffer_bases[rank] + (size_t)rank * rank_stride_bytes)
+                 : nullptr;
+  const uint64_t flags_off = 2ull * nranks * rank_stride_bytes;
+  uint32_t sent[DSDV_MAX_PEERS] = {0}, recvd[DSDV_MAX_PEERS] = {0};
+  const uint64_t base = run_index << 32;
+  auto owner = [&](int s) { return s % nranks; };
+  auto send = [&](int dst, uint64_t t1) -> cudaError_t {
+    ++sent[dst];
+    int32_t *dst_slot = (int32_t *)((char *)buffer_bases[dst] + (size_t)rank * rank_stride_bytes);
+    unsigned long long *dst_flag =
+        (unsigned long long *)((char *)buffer_bases[dst] + flags_off) + rank;
+    return dsdv::launch_hop_send(t1, dst_slot, payload, dst_flag, base | sent[dst], st);
+  };
+  auto recv = [&](int src) -> cudaError_t {
+    ++recvd[src];
+    const unsigned long long *flag =
+        (const unsigned long long *)((char *)buffer_bases[rank] + flags_off) + src;
+    const int32_t *slot = (const int32_t *)((char *)buffer_bases[rank] + (size_t)src * rank_stride_bytes);
+    return dsdv::launch_hop_recv(flag, base | recvd[src], timeout_ns, status, slot, payload, st);
+  };
+  size_t launches = 0;
+  for (int u = 0; u < n_units && e == cudaSuccess; ++u) {
+    for (int s = 0; s < n_stages && e == cudaSuccess; ++s) {
+      if (owner(s) != rank) continue;
+      if (s == 0) {
+        if (compute_ns[u]) {
+          e = dsdv::launch_spin(compute_ns[u], st);  // the unit's compute (k t0 or t0)
+          ++launches;
+        }
+      } else if (owner(s - 1) != rank) {
+        e = recv(owner(s - 1));
+        ++launches;
+      }
+      if (e != cudaSuccess || s == n_stages - 1) continue;
+      if (owner(s + 1) != rank) {
+        e = send(owner(s + 1), t1_ns);  // t1 spin, then the NVLink store
+      } else if (t1_ns) {
+        e = dsdv::launch_spin(t1_ns, st);  // next stage on this GPU: the latency only
+      }
+      ++launches;
+    }
+    // back edge: the committed tokens return to stage 0 for the next unit
+    if (e == cudaSuccess && owner(n_stages - 1) != owner(0)) {
+      if (rank == owner(n_stages - 1)) {
+        e = send(owner(0), 0);
+        ++launches;
+      } else if (rank == owner(0)) {
+        e = recv(owner(n_stages - 1));
+        ++launches;
+      }
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "pipeline hop launch");
+  ctx->launches += launches;
   return DSDV_OK;
 }
 

@@ -679,4 +679,76 @@ cudaError_t launch_tokens_max(const int32_t *tok, size_t stride, int nranks, int
   return cudaGetLastError();
 }
 
+// a timed-out flag round (dsdv_peer_wait status) fails every sequence
+__global__ void status_fold_kernel(const int32_t *peer_status, int32_t *status, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B && *peer_status != 0) status[b] = DSDV_E_NCCL;
+}
+
+cudaError_t launch_status_fold(const int32_t *peer_status, int32_t *status, int batch,
+                               cudaStream_t stream) {
+  status_fold_kernel<<<(batch + 255) / 256, 256, 0, stream>>>(peer_status, status, batch);
+  return cudaGetLastError();
+}
+
+// ---- pipeline emulation hops ----
+// One link of the pipeline: the injected latency t1 (a device spin), then the
+// committed-token payload stored into the next stage's GPU (NVLink peer store
+// into its CUDA-IPC-mapped buffer) and a release of the per-source counter.
+__global__ void hop_send_kernel(unsigned long long t1_ns, int32_t *dst_payload,
+                                const int32_t *payload, unsigned long long *dst_flag,
+                                unsigned long long value) {
+  if (threadIdx.x == 0 && t1_ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < t1_ns);
+  }
+  __syncwarp();
+  if (threadIdx.x < 16) dst_payload[threadIdx.x] = payload[threadIdx.x];
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst_flag), "l"(value) : "memory");
+  }
+}
+
+// The receiving stage: wait for the source's counter, take the payload.
+__global__ void hop_recv_kernel(const unsigned long long *flag, unsigned long long value,
+                                unsigned long long timeout_ns, int *status, const int32_t *slot,
+                                int32_t *payload) {
+  if (threadIdx.x == 0) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      if (v >= value) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        if (status) atomicExch(status, DSDV_E_NCCL);
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
+  __syncwarp();
+  if (threadIdx.x < 16) payload[threadIdx.x] = *(volatile const int32_t *)(slot + threadIdx.x);
+}
+
+cudaError_t launch_hop_send(unsigned long long t1_ns, int32_t *dst_payload, const int32_t *payload,
+                            unsigned long long *dst_flag, unsigned long long value,
+                            cudaStream_t stream) {
+  hop_send_kernel<<<1, 32, 0, stream>>>(t1_ns, dst_payload, payload, dst_flag, value);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hop_recv(const unsigned long long *flag, unsigned long long value,
+                            unsigned long long timeout_ns, int *status, const int32_t *slot,
+                            int32_t *payload, cudaStream_t stream) {
+  hop_recv_kernel<<<1, 32, 0, stream>>>(flag, value, timeout_ns, status, slot, payload);
+  return cudaGetLastError();
+}
+
 }  // namespace dsdv

@@ -85,8 +85,12 @@ def des_total(units: list[Unit], n_nodes: int, t1: float) -> float:
 # ---- the device emulation --------------------------------------------------
 class PipelineEmulator:
     """Runs units over N logical stages on the `comm` ranks (stage s on rank
-    s mod P). `verifier` supplies dsdv_spin on this rank's device; `comm` is a
-    torch.distributed process group wrapper (None for one GPU)."""
+    s mod P). The whole unit loop of a run is enqueued by one C-ABI call
+    (dsdv_pipeline_run): device spins for the compute and the injected link
+    latency, and across GPUs the hops are NVLink peer stores of the committed
+    tokens into the next rank's CUDA-IPC-mapped buffer plus a per-source
+    counter the receiver's stream waits on — no collective and no host round
+    trip per hop. `comm` is a torch.distributed wrapper (None for one GPU)."""
 
     def __init__(self, verifier, n_stages: int, comm=None):
         import torch
@@ -96,52 +100,45 @@ class PipelineEmulator:
         self.comm = comm
         self.P = comm.size if comm else 1
         self.rank = comm.rank if comm else 0
-        self.payload = torch.zeros(16, dtype=torch.int32, device=torch.device("cuda", verifier.device))
+        self.dev = torch.device("cuda", verifier.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.ex = None
+        if self.P > 1:
+            from .sharded import PeerExchange
+            self.ex = PeerExchange(verifier, self.P, self.rank, 64, comm=comm)
+            if not self.ex.ok:
+                raise RuntimeError("pipeline emulation: peer buffers could not be mapped")
+        self.runs = 0
 
     def owner(self, s: int) -> int:
         return s % self.P
 
-    def _send(self, dst: int):
-        self.comm.dist.send(self.payload, dst)
-
-    def _recv(self, src: int):
-        self.comm.dist.recv(self.payload, src)
-
     def run(self, units: list[Unit], t1_ns: int) -> float:
         """Executes the units (compute in ns); returns elapsed device
         milliseconds (max over ranks when distributed)."""
+        import ctypes as C
+        from .dsdv import LIB
         torch = self.torch
-        dev = torch.device("cuda", self.v.device)
         if self.comm:
             self.comm.dist.barrier()
-        torch.cuda.synchronize(dev)
+        torch.cuda.synchronize(self.dev)
+        self.runs += 1
+        compute = (C.c_uint64 * max(1, len(units)))(*[int(u.compute) for u in units])
+        bases = (C.c_void_p * self.P)(*(self.ex.bases if self.ex else [None]))
+        stream = torch.cuda.current_stream(self.dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for u in units:
-            for s in range(self.N):
-                if self.owner(s) != self.rank:
-                    continue
-                if s == 0:
-                    if u.compute > 0:
-                        self.v.spin(int(u.compute))  # the unit's compute (ns)
-                else:
-                    if self.P > 1:
-                        self._recv(self.owner(s - 1))
-                if s < self.N - 1:
-                    self.v.spin(t1_ns)
-                    if self.P > 1:
-                        self._send(self.owner(s + 1))
-            # back edge: the committed tokens return to stage 0 for the next unit
-            if self.P > 1 and self.owner(self.N - 1) != self.owner(0):
-                if self.rank == self.owner(self.N - 1):
-                    self._send(self.owner(0))
-                elif self.rank == self.owner(0):
-                    self._recv(self.owner(self.N - 1))
-        e1.record()
-        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        self.v._check(LIB.dsdv_pipeline_run(
+            self.v._h, self.N, self.P, self.rank, bases, self.ex.stride if self.ex else 0, compute,
+            len(units), int(t1_ns), self.runs, int(60e9), self.status.data_ptr(),
+            stream.cuda_stream))
+        e1.record(stream)
+        torch.cuda.synchronize(self.dev)
+        if int(self.status.item()) != 0:
+            raise RuntimeError("pipeline emulation: a hop timed out")
         ms = e0.elapsed_time(e1)
         if self.comm:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=self.dev)
             self.comm.all_reduce_max(t)
             ms = float(t.item())
         return ms

@@ -328,11 +328,12 @@ class ShardedVerifier:
 
     def _peer_failed(self) -> bool:
         """Did a flag round of an earlier window time out? Read without a sync:
-        the status copy of the last window is checked once it has landed."""
+        the status of the last window's first sequence (a timeout fails every
+        sequence with DSDV_E_NCCL) is checked once it has landed."""
         ev = getattr(self, "_peer_event", None)
         if ev is None or not ev.query():
             return False
-        return int(self._peer_status_host.item()) != 0
+        return int(self._peer_status_host.item()) == dsdv.E_NCCL
 
     # ---- one window on this rank --------------------------------------------
     def verify(self, draft, target, tokens, p: VerifyParams, vocab: int, offset: int, local: int,
@@ -373,27 +374,19 @@ class ShardedVerifier:
                 self._peer_status_host = torch.zeros(1, dtype=torch.int32).pin_memory()
                 self._peer_event = None
             self._epoch += 1
-            w, f = self._epoch, 3 * self._epoch
-            self.stats_peers(ex, w, draft, target, tokens, p, vocab, offset, local, stream,
-                             flag=f)
-            self.wait_peers(ex, f, self._peer_status, stream)
-            out, position, u = self.merge_peers(ex, w, draft, target, tokens, p, vocab, offset,
-                                                local, out, stream)
-            self.signal_peers(ex, f + 1, stream, draft.device)
-            self.wait_peers(ex, f + 1, self._peer_status, stream)
-            self.resolve_peers(ex, w, draft, target, tokens, p, vocab, offset, local, out,
-                               position, u, stream)
-            self.signal_peers(ex, f + 2, stream, draft.device)
-            self.wait_peers(ex, f + 2, self._peer_status, stream)
-            self.tokens_max_peers(ex, w, B, G, M, out.extra_token, stream)
-            # a timed-out flag round fails every sequence of the window (the merged
-            # records may be stale); the caller's sync raises it
-            st = out.status
-            st.copy_(torch.where(self._peer_status.expand_as(st) != 0,
-                                 torch.full_like(st, dsdv.E_NCCL), st))
+            if out is None:
+                out = WindowResult.allocate(B, G, draft.device, True, records=True)
+            # the whole window in one C-ABI call: stats with peer stores, merge,
+            # RESOLVE, tokens max, three flag rounds, timeout -> statuses
+            cp = self._cp(p, draft, target, tokens, vocab, offset, local)
             cs = stream or torch.cuda.current_stream(draft.device)
+            bases = (C.c_void_p * ex.P)(*ex.bases)
+            self.v._check(LIB.dsdv_shard_verify_peers(
+                self.v._h, C.byref(cp), draft.data_ptr(), target.data_ptr(), tokens.data_ptr(),
+                ex.P, ex.rank, bases, ex.stride, self._epoch, int(10e9), C.byref(out._c),
+                cs.cuda_stream))
             with torch.cuda.stream(cs):
-                self._peer_status_host.copy_(self._peer_status, non_blocking=True)
+                self._peer_status_host.copy_(out.status[:1], non_blocking=True)
                 self._peer_event = torch.cuda.Event()
                 self._peer_event.record(cs)
             return out

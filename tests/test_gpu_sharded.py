@@ -121,3 +121,30 @@ def test_peer_exchange_dtypes(verifier, oracle, dtype, P, tau):
                                      torch.equal(a.nan_to_num(7.0), b.nan_to_num(7.0))), k
     rep = compare_window(oracle, d64, t64, toks, got, tau, crit, 11, 0)
     assert rep.ok(), rep.mismatches[:5]
+
+
+def test_pipeline_emulation_across_processes():
+    """C5 on the box's GPUs (stage s on GPU s mod P): the C++-enqueued hop loop
+    (dsdv_pipeline_run, NVLink peer stores + counters) tracks the reference's
+    DES (netsim.cpp:110-172) and the closed form (latency.cpp:81-86)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    n = min(torch.cuda.device_count(), 4)
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    root = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", "29563",
+           str(root / "scripts" / "pipeline_emulation.py"), "--rounds", "32", "--t0-us", "20"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900,
+                       env={**os.environ, "OMP_NUM_THREADS": "1"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 4
+    for d in lines:
+        assert d["gpus"] == n
+        assert abs(d["measured"]["R_comm"] - d["des"]["R_comm"]) < 0.03, d
+        assert d["measured"]["sync_rounds_dsd"] < d["measured"]["sync_rounds_standard"]
