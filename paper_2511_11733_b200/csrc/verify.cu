@@ -87,7 +87,10 @@ __device__ __forceinline__ bool pad_tail(const DevParams &p) {
 __device__ __forceinline__ int vec_index(int h, int warp, int lane) {
   return (warp * kVecs + h) * 32 + lane;
 }
-constexpr int kSlots = 4;
+#ifndef DSDV_SLOTS
+#define DSDV_SLOTS 4
+#endif
+constexpr int kSlots = DSDV_SLOTS;  // items between the compute warps and the epilogue
 // ring depth: 4 x 32 KB stages (3 for fp64 rows, whose slots are larger)
 template <class Acc>
 struct Ring {
@@ -104,16 +107,24 @@ struct Ring {
 // V <= 116 * 2048 = 237,568 for fp64.
 template <class Acc>
 struct Area {
+#ifdef DSDV_TILES  // development probe: smaller slots (2 CTAs per SM)
+  static constexpr int kTiles = DSDV_TILES;
+#else
   static constexpr int kTiles = sizeof(Acc) == 8 ? 1856 : 1024;
+#endif
   static constexpr int kBytes = 8 * kTiles;
 };
-constexpr int kCap = 256;            // captured top-m candidates per row and item
+#ifndef DSDV_KCAP
+#define DSDV_KCAP 256
+#endif
+constexpr int kCap = DSDV_KCAP;      // captured top-m candidates per row and item
 // Sample-request queue. Bound: a request is outstanding from its posting until
 // the epilogue finishes its sample item. Stream items the producer issued but
 // the epilogue has not finished are at most kSlots + kStages (slot reuse and
 // the ring), and between two item boundaries of the producer (where it takes
 // every pending request) the epilogue finishes at most that many regular
-// items, so at most 2 (kSlots + kStages) + kEW < 32 requests are outstanding.
+// items, so at most 2 (kSlots + kStages) + kEW < 32 requests are outstanding:
+// the queue never overflows (no runtime check, no trap).
 #ifndef DSDV_KREQ
 #define DSDV_KREQ 32
 #endif
@@ -1648,16 +1659,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
             else
               want = 2;
           }
-          if (want && vload(&sm.req_tail) - vload(&sm.req_done) >= kReq - kEW) {
-            // cannot happen by the bound above; fail the sequence, never the context
-            *slotp = make_int2(-1, DSDV_E_UNSUPPORTED);
-            if (pair) {
-              __threadfence();
-              st_release(s.flags + (size_t)b * G1 + j, flag_word(p, ev, kOutError));
-            }
-            complete_item(o, s, p, b);
-            want = 0;
-          } else if (want) {
+          if (want) {
             // the flag of a drawing position is published once its draw lands;
             // stash it in the slot until then
             if (pair) *slotp = make_int2(-2, (int)flag_word(p, ev, kOutRejected));
@@ -1910,7 +1912,10 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
 
 // ------------------------------------------------------------------ kernel
 template <class In, bool EE>
-__global__ void __launch_bounds__(kThreads, 1)
+#ifndef DSDV_CTAS
+#define DSDV_CTAS 1  // resident CTAs per SM
+#endif
+__global__ void __launch_bounds__(kThreads, DSDV_CTAS)
     fused_verify_kernel(const __grid_constant__ DevParams p, const In *__restrict__ draft,
                         const In *__restrict__ target, const int32_t *__restrict__ tokens,
                         const __grid_constant__ DevOut o, const __grid_constant__ DevScratch s) {
