@@ -269,7 +269,7 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   s.stop = ctx->stop;
   s.streamed = ctx->streamed;
   s.trace = nullptr;
-#ifdef DSDV_TRACE
+#if defined(DSDV_TRACE) || defined(DSDV_TRACE_LOCAL)
   if (!ctx->trace) {
     cudaMalloc(&ctx->trace, 1024 * dsdv::kTraceWords * sizeof(unsigned long long));
     cudaMemset(ctx->trace, 0, 1024 * dsdv::kTraceWords * sizeof(unsigned long long));
@@ -352,7 +352,7 @@ uint64_t dsdv_launch_count(const dsdv_ctx *ctx) { return ctx ? ctx->launches : 0
 // cycle counters of a DSDV_TRACE build. Returns the number of CTAs, 0 if the
 // library was built without tracing.
 int dsdv_debug_trace(dsdv_ctx *ctx, unsigned long long *host, int max_ctas) {
-#ifdef DSDV_TRACE
+#if defined(DSDV_TRACE) || defined(DSDV_TRACE_LOCAL)
   if (!ctx || !ctx->trace) return 0;
   const int n = max_ctas < 1024 ? max_ctas : 1024;
   cudaDeviceSynchronize();

@@ -135,6 +135,8 @@ constexpr float kFloorM = -1e30f;    // finite "empty" max (keeps (v - m) free o
 enum ItemKind : int { kRegular = 0, kSample = 1, kAborted = 2 };
 // StageMeta::kr bit 8: an early-exit abort stage (no data; ends its item)
 constexpr int kAbortBit = 1 << 8;
+// StageMeta::kr bit 9: the item is a row pair (draft + target), else a target row
+constexpr int kPairBit = 1 << 9;
 
 // Optional cycle accounting per CTA (compile with -DDSDV_TRACE; see
 // scripts/trace_roles.py): where each warp role spends its time.
@@ -145,7 +147,24 @@ enum TraceWord : int {
   kTrTopmFallback, kTrMaxSurv, kTrNeedExact, kTrCapCalls, kTrCapLock, kTrCapCycles,
   kTrComputeLoop, kTrComputeA, kTrComputeB
 };
-#ifdef DSDV_TRACE
+#if defined(DSDV_TRACE_LOCAL)
+// light tracing: per-thread counters in registers, one atomicAdd per word at
+// the end of each role (scripts/trace_roles.py, TRACE_LOCAL=1)
+#define TR_START(v) const long long v = clock64()
+#define TR_ADD(tr, w, v) (trv[w] += (unsigned long long)(clock64() - (v)))
+#define TR_INC(tr, w) (void)0
+#define TR_ACC(tr, w, x) (void)0
+#define TR_MAX(tr, w, x) (void)0
+#define TR_DECL unsigned long long trv[kTraceWords] = {0}
+#define TR_FLUSH(tr)                                              \
+  do {                                                            \
+    if (tr)                                                       \
+      for (int i_ = 0; i_ < kTraceWords; ++i_)                    \
+        if (trv[i_]) atomicAdd((tr) + i_, trv[i_]);               \
+  } while (0)
+#elif defined(DSDV_TRACE)
+#define TR_DECL (void)0
+#define TR_FLUSH(tr) (void)0
 #define TR_START(v) const long long v = clock64()
 #define TR_ADD(tr, w, v)                                                         \
   do {                                                                           \
@@ -164,6 +183,8 @@ enum TraceWord : int {
     if (tr) atomicMax((tr) + (w), (unsigned long long)(x));    \
   } while (0)
 #else
+#define TR_DECL (void)0
+#define TR_FLUSH(tr) (void)0
 #define TR_START(v) (void)0
 #define TR_ADD(tr, w, v) (void)0
 #define TR_INC(tr, w) (void)0
@@ -179,6 +200,7 @@ struct alignas(16) StageMeta {  // one LDS.128 per chunk
   __device__ __forceinline__ int kind() const { return kr & 1; }
   __device__ __forceinline__ int req() const { return (kr >> 1) & 127; }
   __device__ __forceinline__ bool abort() const { return (kr & kAbortBit) != 0; }
+  __device__ __forceinline__ bool pair() const { return (kr & kPairBit) != 0; }
 };
 
 template <class Acc>
@@ -546,7 +568,9 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
                                            int c, ItemState<typename InTraits<In>::Acc> &S,
                                            const DevParams &p, int warp, int lane,
                                            Slot<typename InTraits<In>::Acc> &sl, int *bmax_t,
-                                           int *bmax_d, unsigned long long *trl) {
+                                           int *bmax_d, unsigned long long *trl,
+                                           const uint4 (&pre_t)[kVecs],
+                                           const uint4 (&pre_d)[kVecs]) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
@@ -558,11 +582,10 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
   auto load = [&]() {
 #pragma unroll
     for (int h = 0; h < kVecs; ++h) {
-      const int q = vec_index(h, warp, lane);
-      const uint4 a = lds128(starget + q * 16);
+      const uint4 a = pre_t[h];  // loaded with the stage descriptor (compute_loop)
       unpack(a, vt[h], (In *)nullptr);
       if (PAIR) {
-        const uint4 bb = lds128(sdraft + q * 16);
+        const uint4 bb = pre_d[h];
         unpack(bb, vd[h], (In *)nullptr);
         diff |= (a.x ^ bb.x) | (a.y ^ bb.y) | (a.z ^ bb.z) | (a.w ^ bb.w);
       } else {
@@ -651,6 +674,7 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
 #else
     if (bt >= th0 || bd >= th1) {
 #endif
+      TR_DECL;
       TR_START(tcap);
       if (bt >= th0) capture_row<In, TAIL>(sl, 0, lt, th0, starget, c, tid, lane, p, trl);
       if (bd >= th1) capture_row<In, TAIL>(sl, 1, ld, th1, sdraft, c, tid, lane, p, trl);
@@ -708,7 +732,8 @@ template <class In>
 __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_t *starget,
                                              int chunk, const Weigher<typename InTraits<In>::Acc> &wf,
                                              double *tiles, const DevParams &p, int tid, int warp,
-                                             int lane) {
+                                             int lane, const uint4 (&pre_t)[kVecs],
+                                             const uint4 (&pre_d)[kVecs]) {
   using Acc = typename InTraits<In>::Acc;
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int CH = kRowBytes / (int)sizeof(In);
@@ -722,9 +747,9 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
     const int q = vec_index(h, warp, lane);
     const int id0 = chunk * CH + q * VEC;
     Acc vt[VEC], vd[VEC];
-    unpack(lds128(starget + q * 16), vt, (In *)nullptr);
+    unpack(pre_t[h], vt, (In *)nullptr);
     if (wf.kind != kWeightPlain) {
-      unpack(lds128(sdraft + q * 16), vd, (In *)nullptr);
+      unpack(pre_d[h], vd, (In *)nullptr);
     } else {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) vd[e] = Acc(0);
@@ -755,8 +780,9 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
   bool pair = false;
   int kind = kRegular, n = 0, s = 0;
   unsigned long long *trl = (tid & 31) == 0 ? tr : nullptr;
+  TR_DECL;
   TR_START(tloop);
-#ifdef DSDV_TRACE
+#if defined(DSDV_TRACE) || defined(DSDV_TRACE_LOCAL)
   long long tb = clock64();
 #endif
   for (;;) {
@@ -775,6 +801,15 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       }
     }
 #endif
+    // the chunk's vectors of both rows go out together with the stage
+    // descriptor: their latency overlaps the descriptor's instead of following it
+    uint4 pre_t[kVecs], pre_d[kVecs];
+#pragma unroll
+    for (int h = 0; h < kVecs; ++h) {
+      const int q = vec_index(h, warp, lane);
+      pre_t[h] = lds128(sm.ring[stage][1] + q * 16);
+      pre_d[h] = lds128(sm.ring[stage][0] + q * 16);
+    }
     const StageMeta md = sm.meta[stage];
     if (md.item < 0) {
       // end of stream: one terminating slot per epilogue warp
@@ -786,6 +821,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
         if (lane == 0) mbar_arrive(&sm.part_full[ns]);
       }
       TR_ADD(trl, kTrComputeLoop, tloop);
+      TR_FLUSH(trl);
       break;
     }
     const int c = md.chunk;
@@ -793,8 +829,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       kind = md.kind();
       n = md.n;
       s = n % kSlots;
-      const int j = md.item / p.B;
-      pair = j < p.gamma;
+      pair = md.pair();
       // the slot (partials + block maxima) must be free before this item runs
       TR_START(ts);
       mbar_wait(&sm.part_empty[s], ((n / kSlots) & 1) ^ 1);
@@ -826,21 +861,22 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       if (pair) {
         if (!tail)
           fold_chunk<In, true, NEEDZ, false>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
-                                             sv.bmax[1], trl);
+                                             sv.bmax[1], trl, pre_t, pre_d);
         else
           fold_chunk<In, true, NEEDZ, true>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
-                                            sv.bmax[1], trl);
+                                            sv.bmax[1], trl, pre_t, pre_d);
       } else if (!tail) {
         fold_chunk<In, false, false, false>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
-                                            sv.bmax[1], trl);
+                                            sv.bmax[1], trl, pre_t, pre_d);
       } else {
         fold_chunk<In, false, false, true>(sd, st, tid, c, S, p, warp, lane, sl, sv.bmax[0],
-                                           sv.bmax[1], trl);
+                                           sv.bmax[1], trl, pre_t, pre_d);
       }
     } else {
 #ifndef DSDV_NOFOLD
       sample_chunk<In>(sm.ring[stage][0], sm.ring[stage][1], c, sm.req[md.req()].wf,
-                       reinterpret_cast<double *>(sm.slot[s].area), p, tid, warp, lane);
+                       reinterpret_cast<double *>(sm.slot[s].area), p, tid, warp, lane, pre_t,
+                       pre_d);
 #endif
     }
     TR_ADD(trl, kind == kRegular ? kTrComputeFold : kTrComputeSample, tf);
@@ -857,7 +893,7 @@ __device__ void compute_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPara
       stage = 0;
       phase ^= 1;
     }
-#ifdef DSDV_TRACE
+#if defined(DSDV_TRACE) || defined(DSDV_TRACE_LOCAL)
     tb = clock64();
 #endif
     if (!last) continue;
@@ -1544,6 +1580,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
   const double omt_d = (double)p.omt_f, tau_d = (double)p.tau_f;
   const int nblocks = p.n_chunks * kCW;  // sample tiles (chunk, warp)
   unsigned long long *trl = lane == 0 ? tr : nullptr;
+  TR_DECL;
   for (int n = ew;; n += kEW) {
     const int si = n % kSlots;
     TR_START(tw);
@@ -1758,6 +1795,7 @@ __device__ void epilogue_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
   // peer exchange: this warp's stores into the other ranks' buffers are
   // visible system-wide before the kernel ends (dsdv_peer_signal follows)
   if (o.npeer) __threadfence_system();
+  TR_FLUSH(trl);
 }
 
 // ------------------------------------------------------------------ producer warp
@@ -1769,6 +1807,7 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
                                             unsigned long long &copied, const DevScratch &sx,
                                             const DevParams &pp, int b, int j) {
   constexpr int CH = kRowBytes / (int)sizeof(In);
+  TR_DECL;
   for (int c = 0; c < n_chunks; ++c) {
     TR_START(tw);
     mbar_wait_spin(&sm.empty[stage], phase ^ 1);
@@ -1793,7 +1832,7 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
     m.item = item;
     m.chunk = c;
     m.n = n;
-    m.kr = kind | (req << 1);
+    m.kr = kind | (req << 1) | (two ? kPairBit : 0);
     sm.meta[stage] = m;
     const int rem = nlocal - c * CH;
     const int elems = rem < CH ? rem : CH;
@@ -1830,12 +1869,14 @@ __device__ __forceinline__ void stream_rows(Smem<Acc> &sm, const In *rt,
       phase ^= 1;
     }
   }
+  TR_FLUSH(tr);
 }
 
 template <class In, bool EE>
 __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevParams &p,
                               const In *__restrict__ draft, const In *__restrict__ target,
                               const DevOut &o, const DevScratch &s, unsigned long long *tr) {
+  TR_DECL;
   const int G1 = p.gamma + 1;
   unsigned long long copied = 0;
   int stage = 0;
@@ -1899,6 +1940,7 @@ __device__ void producer_loop(Smem<typename InTraits<In>::Acc> &sm, const DevPar
     TR_ADD(tr, kTrProdDrain, td);
   }
   // end of stream
+  TR_FLUSH(tr);
   if (s.streamed) atomicAdd(s.streamed, copied);
   mbar_wait(&sm.empty[stage], phase ^ 1);
   StageMeta m;
@@ -1925,6 +1967,7 @@ __global__ void __launch_bounds__(kThreads, DSDV_CTAS)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   unsigned long long *tr = s.trace ? s.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
+  TR_DECL;
   TR_START(tk);
 
   if (tid == 0) {
@@ -1950,6 +1993,7 @@ __global__ void __launch_bounds__(kThreads, DSDV_CTAS)
     epilogue_loop<In, EE>(sm, p, draft, target, tokens, o, s, warp - kEpiWarp, lane, tr);
     if (lane == 0 && atomicAdd(&sm.epi_exit, 1) == kEW - 1) {
       TR_ADD(tr, kTrKernel, tk);
+      TR_FLUSH(tr);
       // last CTA out re-arms the work counters for the next launch
       __threadfence();
       const unsigned prev = atomicAdd(s.exit_count, 1u);
