@@ -212,6 +212,11 @@ dsdv_status dsdv_pipeline_run(dsdv_ctx *ctx, int32_t n_stages, int32_t nranks, i
                               uint64_t run_index, uint64_t timeout_ns, int32_t *status,
                               void *stream);
 
+/* In place, on the device: values[i] = ln(values[i]), -inf for zero. The C++
+ * drop-in uploads its fp64 probability rows as they are and turns them into
+ * the logit rows the fused kernel folds (softmax(ln p) = p). Asynchronous. */
+dsdv_status dsdv_log_rows(dsdv_ctx *ctx, double *values, uint64_t count, void *stream);
+
 /* ---- threshold calibration (calibrate.cpp:51-148) ------------------------ */
 typedef struct {
   double ratio_limit, gap_limit, overlap_floor; /* KeyCriteria (verifier.hpp:32-43) */

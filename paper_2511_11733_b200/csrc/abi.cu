@@ -59,6 +59,7 @@ cudaError_t launch_peer_wait(const unsigned long long *flags, int nranks, unsign
                              unsigned long long timeout_ns, int *status, cudaStream_t stream);
 cudaError_t launch_status_fold(const int32_t *peer_status, int32_t *status, int batch,
                                cudaStream_t stream);
+cudaError_t launch_log_rows(double *x, size_t n, cudaStream_t stream);
 cudaError_t launch_hop_send(unsigned long long t1_ns, int32_t *dst_payload, const int32_t *payload,
                             unsigned long long *dst_flag, unsigned long long value,
                             cudaStream_t stream);
@@ -1068,6 +1069,15 @@ dsdv_status dsdv_pipeline_run(dsdv_ctx *ctx, int32_t n_stages, int32_t nranks, i
   }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "pipeline hop launch");
   ctx->launches += launches;
+  return DSDV_OK;
+}
+
+dsdv_status dsdv_log_rows(dsdv_ctx *ctx, double *values, uint64_t count, void *stream) {
+  if (!ctx || (!values && count)) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = dsdv::launch_log_rows(values, (size_t)count, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "log rows launch");
+  ctx->launches += 1;
   return DSDV_OK;
 }
 

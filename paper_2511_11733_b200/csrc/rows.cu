@@ -295,6 +295,26 @@ __global__ void __launch_bounds__(1024) mix_rows_kernel(int kind, int V, const d
   if (threadIdx.x == 0) *status = DSDV_OK;
 }
 
+// In-place natural log of fp64 probability rows (the drop-in's Distribution
+// rows become the logit rows the fused kernel folds: softmax(log p) = p);
+// zero probabilities become -inf.
+__global__ void log_rows_kernel(double *x, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    x[i] = v > 0.0 ? log(v) : -INFINITY;
+  }
+}
+
+cudaError_t launch_log_rows(double *x, size_t n, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 4 * 148) blocks = 4 * 148;
+  log_rows_kernel<<<(unsigned)blocks, 256, 0, stream>>>(x, n);
+  return cudaGetLastError();
+}
+
+
 // Pipeline emulation: one thread holds the stream for `ns`
 // nanoseconds of %globaltimer — a stage's compute step t0 or a link's
 // injected latency t1.

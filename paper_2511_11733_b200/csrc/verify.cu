@@ -425,7 +425,10 @@ __device__ __forceinline__ void capture_row(Slot<Acc> &sl, int r, int lkey, int 
   int *bins = sl.klist[r];
   const int bin = vload(bins + lane);
   if (lkey > bin) atomicMax(bins + lane, lkey);
-  if (__popc(__ballot_sync(0xffffffffu, max(bin, lkey) > th)) >= p.top_m + 8) {
+#ifndef DSDV_CAPSORT
+#define DSDV_CAPSORT 8
+#endif
+  if (__popc(__ballot_sync(0xffffffffu, max(bin, lkey) > th)) >= p.top_m + DSDV_CAPSORT) {
     TR_INC(trl, kTrCapLock);
     __syncwarp();
     const int nth = theta_from_bins(bins, p.top_m, lane);

@@ -152,12 +152,6 @@ void check_token(const Distribution &d, int token, const char *what) {
                          " outside vocabulary of size " + std::to_string(d.size()));
 }
 
-// fp64 log-probability row (the device verifier takes logits; softmax(log p) = p)
-void put_log_row(double *dst, const Distribution &d, int stride) {
-  const size_t V = d.size();
-  for (size_t i = 0; i < V; ++i) dst[i] = d[i] > 0.0 ? std::log(d[i]) : -kInf;
-  for (size_t i = V; i < static_cast<size_t>(stride); ++i) dst[i] = -kInf;
-}
 
 // ---- one window on the device ------------------------------------------
 // rows: gamma draft rows, gamma + 1 target rows, all of one vocabulary.
@@ -242,33 +236,33 @@ struct DeviceWindow {
     }
 
     // stage the rows in pinned memory, one copy
-    const size_t hbytes = (rows_draft + rows_target + (big_m ? 2 * rows_draft : 0)) *
-                              sizeof(double) +
-                          gamma * sizeof(int32_t);
+    // stage the probability rows as they are (pinned, one copy per region); the
+    // device takes their logs (dsdv_log_rows) — no O(V) host transcendentals
+    const size_t hbytes = (rows_draft + rows_target) * sizeof(double) + gamma * sizeof(int32_t);
     char *h = static_cast<char *>(eng.host_arena(hbytes));
     double *hd = reinterpret_cast<double *>(h);
     double *ht = hd + rows_draft;
-    double *hpd = ht + rows_target, *hpt = hpd + (big_m ? rows_draft : 0);
-    int32_t *htok = reinterpret_cast<int32_t *>(hpt + (big_m ? rows_draft : 0));
-    if (big_m) {
-      // probability rows as given (top_ids orders by p, verifier.cpp:40-51)
-      for (int j = 0; j < gamma; ++j) {
-        std::memcpy(hpd + (size_t)j * stride, draft[j]->probs().data(), V * sizeof(double));
-        std::memcpy(hpt + (size_t)j * stride, target[j]->probs().data(), V * sizeof(double));
-        for (int i = V; i < stride; ++i) hpd[(size_t)j * stride + i] = hpt[(size_t)j * stride + i] = 0.0;
-      }
-      cudaMemcpyAsync(d_pd, hpd, rows_draft * sizeof(double), cudaMemcpyHostToDevice, eng.stream);
-      cudaMemcpyAsync(d_pt, hpt, rows_draft * sizeof(double), cudaMemcpyHostToDevice, eng.stream);
-    }
-    for (int j = 0; j < gamma; ++j) put_log_row(hd + (size_t)j * stride, *draft[j], stride);
-    for (int j = 0; j < G1; ++j) put_log_row(ht + (size_t)j * stride, *target[j], stride);
+    int32_t *htok = reinterpret_cast<int32_t *>(ht + rows_target);
+    auto put_row = [&](double *dst, const Distribution &d) {
+      std::memcpy(dst, d.probs().data(), V * sizeof(double));
+      for (int i = V; i < stride; ++i) dst[i] = 0.0;
+    };
+    for (int j = 0; j < gamma; ++j) put_row(hd + (size_t)j * stride, *draft[j]);
+    for (int j = 0; j < G1; ++j) put_row(ht + (size_t)j * stride, *target[j]);
     for (int j = 0; j < gamma; ++j) htok[j] = tokens[j];
-    // d_draft, d_target, d_tokens are carved back to back after 256-B rounding;
-    // copy each region
     cudaMemcpyAsync(d_draft, hd, rows_draft * sizeof(double), cudaMemcpyHostToDevice, eng.stream);
     cudaMemcpyAsync(d_target, ht, rows_target * sizeof(double), cudaMemcpyHostToDevice,
                     eng.stream);
     cudaMemcpyAsync(d_tokens, htok, gamma * sizeof(int32_t), cudaMemcpyHostToDevice, eng.stream);
+    if (big_m) {
+      // top_ids orders by p (verifier.cpp:40-51): keep the probabilities
+      cudaMemcpyAsync(d_pd, d_draft, rows_draft * sizeof(double), cudaMemcpyDeviceToDevice,
+                      eng.stream);
+      cudaMemcpyAsync(d_pt, d_target, rows_draft * sizeof(double), cudaMemcpyDeviceToDevice,
+                      eng.stream);
+    }
+    eng.check(dsdv_log_rows(eng.ctx, d_draft, rows_draft, eng.stream));
+    eng.check(dsdv_log_rows(eng.ctx, d_target, rows_target, eng.stream));
 
     prm.batch = 1;
     prm.gamma = gamma;
