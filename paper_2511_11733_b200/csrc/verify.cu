@@ -727,6 +727,24 @@ __device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t 
   }
 }
 
+// The same fold loading its own vectors (development probes: scripts/micro/).
+template <class In, bool PAIR, bool NEEDZ, bool TAIL>
+__device__ __forceinline__ void fold_chunk(const uint8_t *sdraft, const uint8_t *starget, int tid,
+                                           int c, ItemState<typename InTraits<In>::Acc> &S,
+                                           const DevParams &p, int warp, int lane,
+                                           Slot<typename InTraits<In>::Acc> &sl, int *bmax_t,
+                                           int *bmax_d, unsigned long long *trl) {
+  uint4 pre_t[kVecs], pre_d[kVecs];
+#pragma unroll
+  for (int h = 0; h < kVecs; ++h) {
+    const int q = vec_index(h, warp, lane);
+    pre_t[h] = lds128(starget + q * 16);
+    pre_d[h] = lds128(sdraft + q * 16);
+  }
+  fold_chunk<In, PAIR, NEEDZ, TAIL>(sdraft, starget, tid, c, S, p, warp, lane, sl, bmax_t, bmax_d,
+                                    trl, pre_t, pre_d);
+}
+
 // Sample item: per-tile fp64 sums of the residual / bonus weights. Tile
 // (chunk, warp) covers the warp's contiguous kVecs * 32 vectors of the chunk,
 // ids [chunk*CH + warp*kVecs*32*VEC, +kVecs*32*VEC): tile index order is id
