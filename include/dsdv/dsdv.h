@@ -217,6 +217,10 @@ dsdv_status dsdv_pipeline_run(dsdv_ctx *ctx, int32_t n_stages, int32_t nranks, i
  * the logit rows the fused kernel folds (softmax(ln p) = p). Asynchronous. */
 dsdv_status dsdv_log_rows(dsdv_ctx *ctx, double *values, uint64_t count, void *stream);
 
+/* One process driving several GPUs (no IPC): let ctx's device store into
+ * peer_device's memory over NVLink (cudaDeviceEnablePeerAccess). */
+dsdv_status dsdv_enable_peer_access(dsdv_ctx *ctx, int32_t peer_device);
+
 /* ---- threshold calibration (calibrate.cpp:51-148) ------------------------ */
 typedef struct {
   double ratio_limit, gap_limit, overlap_floor; /* KeyCriteria (verifier.hpp:32-43) */

@@ -1072,6 +1072,24 @@ dsdv_status dsdv_pipeline_run(dsdv_ctx *ctx, int32_t n_stages, int32_t nranks, i
   return DSDV_OK;
 }
 
+dsdv_status dsdv_enable_peer_access(dsdv_ctx *ctx, int32_t peer_device) {
+  if (!ctx) return DSDV_E_INVARIANT;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  int ok = 0;
+  e = cudaDeviceCanAccessPeer(&ok, ctx->device, peer_device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaDeviceCanAccessPeer");
+  if (!ok) return fail(ctx, DSDV_E_UNSUPPORTED, "device %d cannot access device %d", ctx->device,
+                       peer_device);
+  e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    e = cudaSuccess;
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaDeviceEnablePeerAccess");
+  return DSDV_OK;
+}
+
 dsdv_status dsdv_log_rows(dsdv_ctx *ctx, double *values, uint64_t count, void *stream) {
   if (!ctx || (!values && count)) return DSDV_E_INVARIANT;
   cudaError_t e = cudaSetDevice(ctx->device);

@@ -85,6 +85,7 @@ def _load() -> C.CDLL:
         "dsdv_pipeline_run": (st, [vp, C.c_int32, C.c_int32, C.c_int32, vp, C.c_uint64, vp,
                                    C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]),
         "dsdv_log_rows": (st, [vp, vp, C.c_uint64, vp]),
+        "dsdv_enable_peer_access": (st, [vp, C.c_int32]),
         "dsdv_calibrate": (st, [vp, vp, C.c_int32, vp, C.c_int64, vp, C.c_int32, C.c_double,
                                 C.c_int32, C.c_double, vp]),
         "dsdv_window_stats_nm": (st, [vp, C.POINTER(_Params), vp, vp, vp, vp,
@@ -142,7 +143,7 @@ LIB = _load()
 EXPORTED = ("dsdv_create", "dsdv_destroy", "dsdv_last_error", "dsdv_abi_version", "dsdv_validate",
             "dsdv_verify", "dsdv_verify_early_exit", "dsdv_streamed_bytes",
             "dsdv_shard_exchange_bytes", "dsdv_shard_verify_peers", "dsdv_calibrate",
-            "dsdv_pipeline_run", "dsdv_log_rows",
+            "dsdv_pipeline_run", "dsdv_log_rows", "dsdv_enable_peer_access",
             "dsdv_window_stats_nm", "dsdv_norm_match_scratch_bytes", "dsdv_norm_match_rows", "dsdv_window_stats", "dsdv_sample_extra", "dsdv_draft_sample",
             "dsdv_sync", "dsdv_uniform", "dsdv_synth_logits", "dsdv_launch_count",
             "dsdv_shard_stats", "dsdv_shard_merge", "dsdv_shard_sample", "dsdv_mix_rows",
