@@ -467,7 +467,7 @@ __device__ __forceinline__ void capture_row(Slot<Acc> &sl, int r, int lkey, int 
 }
 
 #ifndef DSDV_ZMUFU
-#define DSDV_ZMUFU 3
+#define DSDV_ZMUFU 4
 #endif
 constexpr int kZMufu = DSDV_ZMUFU;
 
