@@ -11,6 +11,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2511_11733_b200.dsdv import Verifier, VerifyParams, WindowResult  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 B, G, V = 1024, 16, 151936
 peak = json.loads((Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").read_text()
@@ -33,16 +34,18 @@ for tau in (0.0, 0.1, 0.2, 0.3, 0.4, 0.5):
             v.verify(draft, target, tokens, p, vocab=V, out=out, early_exit=ee)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for w in range(5):
-            p.window = 100 + w
-            v.verify(draft, target, tokens, p, vocab=V, out=out, early_exit=ee)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 5
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            e0.record()
+            for w in range(20):
+                p.window = 100 + w
+                v.verify(draft, target, tokens, p, vocab=V, out=out, early_exit=ee)
+            e1.record()
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
         v.sync(p, out, batch=B, vocab=V)
         res[mode] = {"ms_per_window": ms, "verified_tokens_per_s": B * G / (ms * 1e-3),
-                     "mean_accepted_k": float(out.accepted_count.float().mean())}
+                     "mean_accepted_k": float(out.accepted_count.float().mean()),
+                     "clocks": clk.summary()}
         if not ee:
             res[mode]["GBps"] = nbytes / (ms * 1e-3) / 1e9
             res[mode]["frac_of_measured_hbm"] = res[mode]["GBps"] / peak
