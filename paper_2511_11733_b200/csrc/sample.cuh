@@ -192,7 +192,8 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
                                        int n, double u, double eps, SampleShared *sh, int tid,
                                        int *near_out, double t_override = -1.0,
                                        double *tiles_out = nullptr,
-                                       const double *tiles_in = nullptr) {
+                                       const double *tiles_in = nullptr,
+                                       bool mass_only = false, int min_g = 1) {
   constexpr int VEC = InTraits<In>::kVec;
   constexpr int U = 4;  // tiles in flight per warp
   const Weigher<Acc> wf = wf_s;
@@ -200,7 +201,9 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
   const int warp = tid >> 5, lane = tid & 31;
   const int sub = 32 * VEC;                          // elements per sub-tile
   const int nsub = (n + sub - 1) / sub;
-  const int G = (nsub + kMaxTiles - 1) / kMaxTiles;  // sub-tiles per tile
+  // sub-tiles per tile (min_g > 1: fewer, longer tiles for short rows, fewer
+  // per-tile reductions; every pass over the same row must use the same value)
+  const int G = max(min_g, (nsub + kMaxTiles - 1) / kMaxTiles);
   const int ntiles = (nsub + G - 1) / G;
   const int per_warp = (ntiles + kConsumerWarps - 1) / kConsumerWarps;
   const int t0 = min(ntiles, warp * per_warp);
@@ -309,7 +312,7 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
       sh->W = W;
       sh->T = T;
       sh->base = base;
-      sh->crossing_tile = (W > 0.0) ? found : -1;
+      sh->crossing_tile = (W > 0.0 && !mass_only) ? found : -1;
       sh->result = (W > 0.0) ? L : -1;  // rounding-gap fallback: last supported id
       sh->near = (W > 0.0 && found < 0) ? 1 : 0;
     }

@@ -29,8 +29,6 @@
 namespace dsdv {
 
 constexpr int kMaxShards = 64;
-constexpr int kStageCand = 128;  // staged slice candidates per row (P * top_m)
-constexpr int kStageWarps = 16;  // positions staged (gamma + 1 <= 16)
 
 struct MergeIn {
   const double *rec;   // rank 0's [B][G1][kRecordWords] partial records
@@ -42,12 +40,15 @@ struct MergeIn {
   size_t rec_stride, topv_stride, topi_stride;
 };
 
-// One CTA per sequence, one warp per position (max(256, 32 (gamma+1))
-// threads): each warp merges its position's P slice records with warp
-// reductions and the top-m overlap with a warp-parallel ranking, lane 0 runs
-// the fp64 decision; warp 0 then finds the first rejection (verifier.cpp:
-// 223-250), and the CTA's first 256 threads compute this slice's mass of the
-// extra-draw row (the MASS step of dsdv_shard_sample, fused).
+// One warp per sequence, one lane per position j in [0, gamma] (the decide
+// step of the merge): lane j combines its position's P slice records in shard
+// order (log-sum-exp of the slice normalisers), merges the P sorted slice
+// top-m lists of both rows (a P-way merge by (value desc, id asc), the order of
+// top_ids), evaluates is_key / soften / accept_prob (verifier.cpp:136-196) in
+// fp64 and draws its Philox accept uniform; the warp then finds the first
+// rejection (:223-250) with one ballot. Identical inputs give identical
+// decisions on every rank. The extra-draw mass (MASS) is a separate streaming
+// pass (shard_sample_kernel, mode 0).
 struct PosSummary {
   int err, key, kind, near, accepted;
 };
@@ -64,378 +65,329 @@ __device__ __forceinline__ void put_peers(T *a, T v, const PeerDelta &pd) {
   for (int q = 0; q < pd.n; ++q) *reinterpret_cast<T *>(reinterpret_cast<char *>(a) + pd.d[q]) = v;
 }
 
-// MAXT: the block size bound the registers are sized for (gamma + 1 <= 10
-// position warps fit 320 threads and four CTAs per SM; larger gamma uses 1024)
-template <class In, int MAXT = 1024, int MINB = 1>
-__global__ void __launch_bounds__(MAXT, MINB)
-    shard_merge_kernel(const __grid_constant__ DevParams p, const MergeIn in,
-                       const In *__restrict__ draft, const In *__restrict__ target,
-                       const int32_t *__restrict__ tokens, const DevOut o,
-                       int32_t *__restrict__ position, double *__restrict__ uniform,
-                       double *__restrict__ mass_out, double *__restrict__ tiles,
-                       const PeerDelta mpd) {
-  using Acc = typename InTraits<In>::Acc;
-  __shared__ PosSummary summ[32];
-  __shared__ int tset[32][kMaxTopM];
-  // one row's P slice lists staged per warp (P * M <= kStageCand)
-  __shared__ double cand_v[kStageWarps][kStageCand];
-  __shared__ int cand_i[kStageWarps][kStageCand];
-  __shared__ SampleShared samp;
-  __shared__ Weigher<Acc> wf;
-  __shared__ int s_pos;
-  const int b = blockIdx.x;
+constexpr int kDecideWarps = 4;  // sequences per CTA
+constexpr size_t kDecideStageMax = 160 * 1024;  // dynamic shared memory for staged lists
+constexpr int kSliceTileSubs = 4;  // MASS / RESOLVE tiles: >= 4 sub-tiles (1-2K ids)
+
+// One row's P sorted slice lists: entry h of slice q at v[q * qs + h] (values)
+// and id[q * qs + h] (ids); shared memory when the warp staged them, else the
+// exchange buffer itself.
+struct SliceLists {
+  const double *v;
+  const int32_t *id;
+  size_t qs_v, qs_i;
+};
+
+// Lane-local P-way merge of one row's sorted slice lists (P <= PMAX; with
+// PMAX = 8 the list heads stay in registers): calls emit(k, id) for the top M
+// in order (slices shorter than M leave id -1 entries, which end a list).
+template <int PMAX, class Emit>
+__device__ __forceinline__ void merge_slice_lists(const SliceLists &L, int P, int M, Emit emit) {
+  int heads[PMAX], hid[PMAX];
+  double hv[PMAX];
+#pragma unroll
+  for (int q = 0; q < PMAX; ++q) {
+    heads[q] = 0;
+    hid[q] = (q < P && M > 0) ? L.id[q * L.qs_i] : -1;
+    hv[q] = hid[q] >= 0 ? L.v[q * L.qs_v] : 0.0;
+  }
+  for (int n = 0; n < M; ++n) {
+    int bq = -1, bid = 0;
+    double bv = 0.0;
+#pragma unroll
+    for (int q = 0; q < PMAX; ++q) {
+      const int id = hid[q];
+      if (id >= 0 && (bq < 0 || hv[q] > bv || (hv[q] == bv && id < bid))) {
+        bq = q;
+        bv = hv[q];
+        bid = id;
+      }
+    }
+    if (bq < 0) break;  // every list exhausted
+    emit(n, bid);
+    // advance list bq: predicated selects, one load pair at a computed address
+    int h = 0;
+#pragma unroll
+    for (int q = 0; q < PMAX; ++q) {
+      heads[q] += (q == bq) ? 1 : 0;
+      h = (q == bq) ? heads[q] : h;
+    }
+    const int nid = h < M ? L.id[bq * L.qs_i + h] : -1;
+    const double nv = nid >= 0 ? L.v[bq * L.qs_v + h] : 0.0;
+#pragma unroll
+    for (int q = 0; q < PMAX; ++q) {
+      hid[q] = (q == bq) ? nid : hid[q];
+      hv[q] = (q == bq) ? nv : hv[q];
+    }
+  }
+}
+
+template <int PMAX>
+__global__ void __launch_bounds__(kDecideWarps * 32)
+    shard_decide_kernel(const __grid_constant__ DevParams p, const MergeIn in,
+                        const int32_t *__restrict__ tokens, const DevOut o,
+                        int32_t *__restrict__ position, double *__restrict__ uniform,
+                        size_t stage_bytes) {
+  __shared__ int tsel_s[kDecideWarps][kMaxTopM][32];  // target top-M ids per lane
+  // staged slice lists of the warp's sequence ([P][gamma][2][M] values, then ids)
+  extern __shared__ __align__(16) unsigned char stage_dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kDecideWarps + warp;
+  if (b >= p.B) return;  // warp-uniform
   const int G = p.gamma, G1 = G + 1, M = p.top_m;
+  const int GM2 = G * 2 * M;
+  double *sv = reinterpret_cast<double *>(stage_dsm + (size_t)warp * stage_bytes);
+  int32_t *si = reinterpret_cast<int32_t *>(sv + (size_t)in.P * GM2);
+  if (stage_bytes) {
+    // one coalesced pass over this sequence's lists in every slice (the
+    // merges below then read shared memory, not dependent global loads)
+    // (eight loads per lane in flight: loads first, then the stores)
+    const int total = in.P * GM2;
+    for (int t0 = 0; t0 < total; t0 += 8 * 32) {
+      double v[8];
+      int32_t id[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = t0 + k * 32 + lane;
+        if (t < total) {
+          const int q = t / GM2, e = t - q * GM2;
+          v[k] = __ldg(in.topv + q * in.topv_stride + (size_t)b * GM2 + e);
+          id[k] = __ldg(in.topi + q * in.topi_stride + (size_t)b * GM2 + e);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = t0 + k * 32 + lane;
+        if (t < total) {
+          sv[t] = v[k];
+          si[t] = id[k];
+        }
+      }
+    }
+    __syncwarp();
+  }
   const double omt = (double)p.omt_f, tau = (double)p.tau_f;
-  if (warp < G1) {
-    const int j = warp;
-    const bool pair = j < G;
-    // ---- normalisers: lanes over slices, log-sum-exp by warp reduction ----
-    double lt = -INFINITY, ld = -INFINITY, lz = -INFINITY, mtq = -INFINITY, mdq = -INFINITY;
-    double lty = NAN, ldy = NAN;
-    int f = 0;
-    for (int q = lane; q < in.P; q += 32) {
-      const double *r = in.rec + q * in.rec_stride + ((size_t)b * G1 + j) * kRecordWords;
-      // running log-sum-exp over this lane's slices (the first one is exact:
-      // log(0 + e^0) = 0, so it is taken as is, without the transcendentals)
-      auto lse2 = [](double acc, double a) -> double {
-        if (acc == -INFINITY) return a;
-        const double m = fmax(acc, a);
-        return m == -INFINITY ? -(double)INFINITY : m + log(exp(acc - m) + exp(a - m));
-      };
+  // gamma + 1 <= 16: two lanes per position, lane j (target side and the
+  // decision) and lane j + 16 (draft side), so the two P-way merges and the
+  // normalisers of the two rows run side by side; otherwise one lane does both
+  const bool split = G1 <= 16;
+  const int j = split ? (lane & 15) : lane;
+  const bool tside = !split || lane < 16, dside = !split || lane >= 16;
+  const bool pair = j < G;
+  const double *r0 = in.rec + ((size_t)b * G1 + (j < G1 ? j : 0)) * kRecordWords;
+  int(*tsel)[32] = tsel_s[warp];
+  SliceLists L{};
+  if (pair) {
+    if (stage_bytes) {
+      L = SliceLists{sv + (size_t)j * 2 * M, si + (size_t)j * 2 * M, (size_t)GM2, (size_t)GM2};
+    } else {
+      const size_t lo = ((size_t)b * G + j) * 2 * M;
+      L = SliceLists{in.topv + lo, in.topi + lo, in.topv_stride, in.topi_stride};
+    }
+  }
+  // ---- target side: LSE_t in shard order, the owner of y, target top-M ----
+  double mt = -INFINITY, lse_t = -INFINITY, lt_y = NAN, ld_y = NAN;
+  int f = 0, owner = -1, nt = 0;
+  if (j < G1 && tside) {
+    double xt = -INFINITY;
+#pragma unroll(PMAX <= 8 ? PMAX : 1)
+    for (int q = 0; q < PMAX; ++q) {
+      if (q >= in.P) break;
+      const double *r = r0 + q * in.rec_stride;
       const double a_t = r[0] + r[1];
-      if (a_t > -INFINITY) mtq = fmax(mtq, r[0]);
-      lt = lse2(lt, a_t);
+      if (a_t > -INFINITY) mt = fmax(mt, r[0]);
+      xt = fmax(xt, a_t);
       if (pair) {
-        const double a_d = r[2] + r[3];
-        if (a_d > -INFINITY) mdq = fmax(mdq, r[2]);
-        ld = lse2(ld, a_d);
-        const double a_z = omt * r[0] + tau * r[2] + r[4];
-        lz = lse2(lz, a_z);
         const int fl = (int)r[7];
         f |= fl;
-        if (fl & 2) {
-          lty = r[5];
-          ldy = r[6];
-        }
+        if ((fl & 2) && owner < 0) owner = q;
       }
     }
-    auto warp_lse = [&](double x) -> double {
-      double m = x;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (m == -INFINITY) return -(double)INFINITY;
-      double e = (x == -INFINITY) ? 0.0 : exp(x - m);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-      return m + log(e);
-    };
-    auto warp_max = [&](double x) -> double {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
-      return x;
-    };
-    const double lse_t = warp_lse(lt), lse_d = warp_lse(ld), lse_z = warp_lse(lz);
-    const double mt = warp_max(mtq), md = warp_max(mdq);
-    const unsigned diffq = __ballot_sync(0xffffffffu, (f & 1) != 0);
-    const unsigned ownq = __ballot_sync(0xffffffffu, (f & 2) != 0);
-    const int owner = ownq ? __ffs(ownq) - 1 : 0;
-    const double lt_y0 = __shfl_sync(0xffffffffu, lty, owner);
-    const double ld_y0 = __shfl_sync(0xffffffffu, ldy, owner);
-    // ---- top-m overlap: rank every slice candidate against all others ----
-    int shared = 0;
+    double et = 0.0;
+    for (int q = 0; q < in.P; ++q) {
+      const double a_t = r0[q * in.rec_stride] + r0[q * in.rec_stride + 1];
+      if (a_t > -INFINITY) et += exp(a_t - xt);
+    }
+    lse_t = xt == -INFINITY ? -(double)INFINITY : xt + log(et);
+    if (owner >= 0) {
+      lt_y = r0[owner * in.rec_stride + 5];
+      ld_y = r0[owner * in.rec_stride + 6];
+    }
+    if (pair)
+      merge_slice_lists<PMAX>(L, in.P, M, [&](int k, int id) {
+        tsel[k][lane] = id;
+        nt = k + 1;
+      });
+  }
+  // ---- draft side: LSE_d, LSE_z in shard order, draft top-M ----
+  double md = -INFINITY, lse_d = -INFINITY, lse_z = -INFINITY;
+  int nd = 0, shared = 0;
+  if (pair && dside) {
+    double xd = -INFINITY, xz = -INFINITY;
+#pragma unroll(PMAX <= 8 ? PMAX : 1)
+    for (int q = 0; q < PMAX; ++q) {
+      if (q >= in.P) break;
+      const double *r = r0 + q * in.rec_stride;
+      const double a_d = r[2] + r[3];
+      if (a_d > -INFINITY) md = fmax(md, r[2]);
+      xd = fmax(xd, a_d);
+      xz = fmax(xz, omt * r[0] + tau * r[2] + r[4]);
+    }
+    double ed = 0.0, ez = 0.0;
+    for (int q = 0; q < in.P; ++q) {
+      const double *r = r0 + q * in.rec_stride;
+      const double a_d = r[2] + r[3];
+      if (a_d > -INFINITY) ed += exp(a_d - xd);
+      const double a_z = omt * r[0] + tau * r[2] + r[4];
+      if (a_z > -INFINITY) ez += exp(a_z - xz);
+    }
+    lse_d = xd == -INFINITY ? -(double)INFINITY : xd + log(ed);
+    lse_z = xz == -INFINITY ? -(double)INFINITY : xz + log(ez);
+    L.v += M;
+    L.id += M;
+    if (split) {
+      merge_slice_lists<PMAX>(L, in.P, M, [&](int k, int id) {
+        tsel[k][lane] = id;  // column j + 16
+        nd = k + 1;
+      });
+    } else {
+      merge_slice_lists<PMAX>(L, in.P, M, [&](int, int id) {
+        bool hit = false;
+        for (int i = 0; i < nt; ++i) hit |= tsel[i][lane] == id;
+        shared += hit ? 1 : 0;
+      });
+    }
+  }
+  __syncwarp();
+  if (split) {
+    const int src = (lane & 15) + 16;
+    md = __shfl_sync(0xffffffffu, md, src);
+    lse_d = __shfl_sync(0xffffffffu, lse_d, src);
+    lse_z = __shfl_sync(0xffffffffu, lse_z, src);
+    nd = __shfl_sync(0xffffffffu, nd, src);
+    if (pair && tside)
+      for (int k = 0; k < nd; ++k) {
+        const int id = tsel[k][lane + 16];
+        bool hit = false;
+        for (int i = 0; i < nt; ++i) hit |= tsel[i][lane] == id;
+        shared += hit ? 1 : 0;
+      }
+  }
+  PosSummary sj{0, 0, DSDV_EFF_TARGET, 0, 1};
+  if (j < G1 && tside) {
+    // ---- decision (fp64) ----
+    int err = 0, key = 0, kind = DSDV_EFF_TARGET, near = 0, accepted = 0;
+    PosEval ev;
+    ev.mt = mt;
+    ev.lst = lse_t - mt;
+    ev.md = pair ? md : 0.0;
+    ev.lsd = pair ? lse_d - md : 0.0;
+    ev.lsz = 0.0;
+    ev.h_t = ev.h_d = ev.p_t_y = ev.p_d_y = ev.nm = ev.p_eff = ev.a = ev.u = 0.0;
+    if (!(lse_t > -INFINITY && isfinite(lse_t))) err = DSDV_E_INVARIANT;
     if (pair) {
-      const int nc = in.P * M;
-      const size_t lo = ((size_t)b * G + j) * 2 * M;
-      const bool staged = nc <= kStageCand && warp < kStageWarps;
-      if (staged && in.P <= 32) {
-        // P-way merge of the sorted slice lists: lane q holds the head of
-        // list q, M warp arg-max steps (value desc, id asc) give the top M
-        for (int r = 0; r < 2; ++r) {
-          for (int c = lane; c < nc; c += 32) {
-            const int q = c / M, i = c - q * M;
-            const int id = in.topi[q * in.topi_stride + lo + r * M + i];
-            cand_i[warp][c] = id;
-            cand_v[warp][c] = id >= 0 ? in.topv[q * in.topv_stride + lo + r * M + i] : 0.0;
-          }
-          if (r == 0 && lane < M) tset[warp][lane] = -1;
-          __syncwarp();
-          int head = 0;
-          for (int k = 0; k < M; ++k) {
-            int bid = -1, bl = 32;
-            if (sizeof(Acc) == 4) {
-              // fp32 logits: (value desc, id asc) as one 64-bit key, a
-              // branch-free warp max (0 = empty, below every real key)
-              unsigned long long key = 0ull;
-              if (lane < in.P && head < M) {
-                const int id = cand_i[warp][lane * M + head];
-                if (id >= 0) {
-                  const unsigned fb = __float_as_uint((float)cand_v[warp][lane * M + head]);
-                  const unsigned ord = (fb & 0x80000000u) ? ~fb : (fb | 0x80000000u);
-                  key = ((unsigned long long)ord << 32) | (unsigned)(~id);
-                }
-              }
-              unsigned long long best = key;
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-                best = other > best ? other : best;
-              }
-              if (best != 0ull) {
-                bid = (int)~(unsigned)best;
-                const unsigned who = __ballot_sync(0xffffffffu, key == best);
-                bl = __ffs(who) - 1;
-              }
-            } else {
-              double bv = -INFINITY;
-              if (lane < in.P && head < M) {
-                const int id = cand_i[warp][lane * M + head];
-                if (id >= 0) {
-                  bv = cand_v[warp][lane * M + head];
-                  bid = id;
-                  bl = lane;
-                }
-              }
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
-                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-                if (ol < 32 && (bl == 32 || ov > bv || (ov == bv && oid < bid))) {
-                  bv = ov;
-                  bid = oid;
-                  bl = ol;
-                }
-              }
-            }
-            if (bl == 32) break;  // every list exhausted (slices shorter than M)
-            if (lane == bl) ++head;
-            if (r == 0) {
-              if (lane == 0) tset[warp][k] = bid;
-            } else {
-              __syncwarp();
-              shared += __ballot_sync(0xffffffffu, lane < M && tset[warp][lane] == bid) ? 1 : 0;
-            }
-          }
-          __syncwarp();
-        }
-      } else
-      for (int r = 0; r < 2; ++r) {  // 0: target, 1: draft
-        if (staged) {
-          // the P sorted lists of this row into shared memory (one coalesced
-          // pass), so the ranking below reads no global memory
-          for (int c = lane; c < nc; c += 32) {
-            const int q = c / M, i = c - q * M;
-            const int id = in.topi[q * in.topi_stride + lo + r * M + i];
-            cand_i[warp][c] = id;
-            cand_v[warp][c] = id >= 0 ? in.topv[q * in.topv_stride + lo + r * M + i] : 0.0;
-          }
-          __syncwarp();
-        }
-        for (int c = lane; c < ((nc + 31) & ~31); c += 32) {
-          const bool val = c < nc;
-          const int q = val ? c / M : 0, i = val ? c - (c / M) * M : 0;
-          int id;
-          double v;
-          if (staged) {
-            id = val ? cand_i[warp][c] : -1;
-            v = val && id >= 0 ? cand_v[warp][c] : 0.0;
-          } else {
-            id = val ? in.topi[q * in.topi_stride + lo + r * M + i] : -1;
-            v = val && id >= 0 ? in.topv[q * in.topv_stride + lo + r * M + i] : 0.0;
-          }
-          int rank = 0;
-          if (id >= 0) {
-            for (int qq = 0; qq < in.P; ++qq) {
-              if (qq == q) {
-                rank += i;  // own list is sorted: its first i entries beat it
-                continue;
-              }
-              for (int ii = 0; ii < M; ++ii) {
-                int id2;
-                double v2;
-                if (staged) {
-                  id2 = cand_i[warp][qq * M + ii];
-                  if (id2 < 0) break;
-                  v2 = cand_v[warp][qq * M + ii];
-                } else {
-                  id2 = in.topi[qq * in.topi_stride + lo + r * M + ii];
-                  if (id2 < 0) break;
-                  v2 = in.topv[qq * in.topv_stride + lo + r * M + ii];
-                }
-                if (!(v2 > v || (v2 == v && id2 < id))) break;  // sorted: no later entry beats it
-                ++rank;
-              }
-            }
-          }
-          const bool top = id >= 0 && rank < M;
-          if (r == 0) {
-            if (top) tset[warp][rank] = id;
-          } else {
-            __syncwarp();
-            bool hit = false;
-            if (top)
-              for (int k = 0; k < M; ++k) hit |= tset[warp][k] == id;
-            shared += __popc(__ballot_sync(0xffffffffu, hit));
-          }
-        }
-        __syncwarp();  // the staged lists are overwritten by the next row
-        if (r == 0) {
-          // fewer than M valid candidates: the rest of the set stays unmatched
-          __syncwarp();
-        }
-      }
-    }
-    if (lane == 0) {
-      int err = 0, key = 0, kind = DSDV_EFF_TARGET, near = 0, accepted = 0;
-      double lt_y = lt_y0, ld_y = ld_y0;
-      PosEval ev;
-      ev.mt = mt;
-      ev.lst = lse_t - mt;
-      ev.md = pair ? md : 0.0;
-      ev.lsd = pair ? lse_d - md : 0.0;
-      ev.lsz = 0.0;
-      ev.h_t = ev.h_d = ev.p_t_y = ev.p_d_y = ev.nm = ev.p_eff = ev.a = ev.u = 0.0;
-      if (!(lse_t > -INFINITY && isfinite(lse_t))) err = DSDV_E_INVARIANT;
-      if (pair) {
-        if (!(lse_d > -INFINITY && isfinite(lse_d)) && !err) err = DSDV_E_INVARIANT;
-        const int y = tokens[(size_t)b * G + j];
-        if (!(ownq && y >= 0 && y < p.V) && !err) err = DSDV_E_INVARIANT;  // check_token_in_vocab
-        if (!ownq) lt_y = ld_y = -INFINITY;
-        ev.nm = (double)shared / (double)M;
-        ev.h_t = (lt_y == -INFINITY) ? INFINITY : lse_t - lt_y;
-        ev.h_d = (ld_y == -INFINITY) ? INFINITY : lse_d - ld_y;
-        ev.p_t_y = exp(lt_y - lse_t);
-        ev.p_d_y = exp(ld_y - lse_d);
-        const bool certain = ev.h_t < kCertainSurprisal;
-        const bool ratio_cert = ev.h_d > 0.0;
-        const bool ratio_rel = ev.h_d / ev.h_t > p.ratio_limit;
-        const bool ratio = certain ? ratio_cert : ratio_rel;
-        const double gap = fabs(ev.p_t_y - ev.p_d_y);
-        key = (ratio || gap > p.gap_limit || ev.nm < p.overlap_floor) ? 1 : 0;
-        const double el = p.eps_lambda;
-        if (ev.h_t < 1e-6 && (ratio_cert != ratio_rel || ev.h_d < 1e-6)) near = 1;
-        if (isfinite(p.ratio_limit) && ev.h_t >= 1e-6 && isfinite(ev.h_d) &&
-            fabs(ev.h_d / ev.h_t - p.ratio_limit) < el * fmax(1.0, p.ratio_limit))
-          near = 1;
-        if (fabs(gap - p.gap_limit) < el * fmax(1.0, p.gap_limit)) near = 1;
-        if (key || p.tau == 0.0 || diffq == 0)
-          kind = DSDV_EFF_TARGET;
-        else if (p.tau == 1.0)
-          kind = DSDV_EFF_DRAFT;
-        else
-          kind = DSDV_EFF_SOFTENED;
-        double p_eff = ev.p_t_y;
-        if (kind == DSDV_EFF_DRAFT) p_eff = ev.p_d_y;
-        if (kind == DSDV_EFF_SOFTENED && !err) {
-          if (lse_z == -INFINITY) {
-            err = DSDV_E_DEGENERATE_MIXTURE;  // disjoint supports (verifier.cpp:181-184)
-          } else {
-            ev.lsz = lse_z - (omt * ev.mt + tau * ev.md);
-            p_eff = exp((1.0 - p.tau) * lt_y + p.tau * ld_y - lse_z);
-          }
-        }
-        if (!err && !(ev.p_d_y > 0.0)) err = DSDV_E_DRAFTING_CONTRACT;
-        ev.p_eff = p_eff;
-        ev.a = err ? 0.0 : fmin(1.0, p_eff / ev.p_d_y);
-        ev.u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b,
-                                   (uint32_t)(G + j));
-        accepted = (!err && ev.u < ev.a) ? 1 : 0;
-        if (!err && fabs(ev.u - ev.a) < p.eps_u) near = 1;
-        const size_t pos = (size_t)b * G + j;
-        if (o.key_mask) o.key_mask[pos] = (uint8_t)key;
-        if (o.accepted) o.accepted[pos] = (uint8_t)accepted;
-        if (o.accept_prob) o.accept_prob[pos] = ev.a;
-        if (o.h_target) o.h_target[pos] = ev.h_t;
-        if (o.h_draft) o.h_draft[pos] = ev.h_d;
-        if (o.p_target_y) o.p_target_y[pos] = ev.p_t_y;
-        if (o.p_draft_y) o.p_draft_y[pos] = ev.p_d_y;
-        if (o.norm_match) o.norm_match[pos] = ev.nm;
-        if (o.p_effective_y) o.p_effective_y[pos] = ev.p_eff;
-        if (o.uniform) o.uniform[pos] = ev.u;
-      }
-      double *rr = o.records + ((size_t)b * G1 + j) * kRecordWords;
-      rr[kRecMt] = ev.mt;
-      rr[kRecLst] = ev.lst;
-      rr[kRecMd] = ev.md;
-      rr[kRecLsd] = ev.lsd;
-      rr[kRecLsz] = ev.lsz;
-      rr[kRecFlags] = (double)(kind | (err << 8) | (key << 16));
-      summ[j] = PosSummary{err, key, kind, near, accepted};
-    }
-  }
-  __syncthreads();
-  // ---- first rejection or error, left to right (verifier.cpp:223-250) ----
-  if (warp == 0) {
-    const bool act = lane < G;
-    const PosSummary sj = act ? summ[lane] : PosSummary{0, 0, 0, 0, 1};
-    const unsigned stop = __ballot_sync(0xffffffffu, act && (sj.err || !sj.accepted));
-    const int k = stop ? __ffs(stop) - 1 : G;
-    const unsigned upto = (k >= 31) ? 0xffffffffu : ((1u << (k + 1)) - 1u);
-    const int keys = __popc(__ballot_sync(0xffffffffu, act && sj.key) & upto);
-    const int nears = __popc(__ballot_sync(0xffffffffu, act && sj.near) & upto);
-    if (lane == 0) {
-      int st = DSDV_OK, pos = -1;
-      double u = 0.0;
-      if (k < G) {
-        if (summ[k].err) {
-          st = summ[k].err;
-        } else if (summ[k].kind == DSDV_EFF_DRAFT) {
-          st = DSDV_E_EMPTY_RESIDUAL;  // residual of P_d against itself (verifier.cpp:209-211)
+      if (!(lse_d > -INFINITY && isfinite(lse_d)) && !err) err = DSDV_E_INVARIANT;
+      const int y = tokens[(size_t)b * G + j];
+      const bool own = owner >= 0;
+      if (!(own && y >= 0 && y < p.V) && !err) err = DSDV_E_INVARIANT;  // check_token_in_vocab
+      if (!own) lt_y = ld_y = -INFINITY;
+      ev.nm = (double)shared / (double)M;
+      ev.h_t = (lt_y == -INFINITY) ? INFINITY : lse_t - lt_y;
+      ev.h_d = (ld_y == -INFINITY) ? INFINITY : lse_d - ld_y;
+      ev.p_t_y = exp(lt_y - lse_t);
+      ev.p_d_y = exp(ld_y - lse_d);
+      const bool certain = ev.h_t < kCertainSurprisal;
+      const bool ratio_cert = ev.h_d > 0.0;
+      const bool ratio_rel = ev.h_d / ev.h_t > p.ratio_limit;
+      const bool ratio = certain ? ratio_cert : ratio_rel;
+      const double gap = fabs(ev.p_t_y - ev.p_d_y);
+      key = (ratio || gap > p.gap_limit || ev.nm < p.overlap_floor) ? 1 : 0;
+      const double el = p.eps_lambda;
+      if (ev.h_t < 1e-6 && (ratio_cert != ratio_rel || ev.h_d < 1e-6)) near = 1;
+      if (isfinite(p.ratio_limit) && ev.h_t >= 1e-6 && isfinite(ev.h_d) &&
+          fabs(ev.h_d / ev.h_t - p.ratio_limit) < el * fmax(1.0, p.ratio_limit))
+        near = 1;
+      if (fabs(gap - p.gap_limit) < el * fmax(1.0, p.gap_limit)) near = 1;
+      if (key || p.tau == 0.0 || (f & 1) == 0)
+        kind = DSDV_EFF_TARGET;
+      else if (p.tau == 1.0)
+        kind = DSDV_EFF_DRAFT;
+      else
+        kind = DSDV_EFF_SOFTENED;
+      double p_eff = ev.p_t_y;
+      if (kind == DSDV_EFF_DRAFT) p_eff = ev.p_d_y;
+      if (kind == DSDV_EFF_SOFTENED && !err) {
+        if (lse_z == -INFINITY) {
+          err = DSDV_E_DEGENERATE_MIXTURE;  // disjoint supports (verifier.cpp:181-184)
         } else {
-          pos = k;
-          u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b,
-                                  (uint32_t)(G + k + 1));
+          ev.lsz = lse_z - (omt * ev.mt + tau * ev.md);
+          p_eff = exp((1.0 - p.tau) * lt_y + p.tau * ld_y - lse_z);
         }
-      } else if (summ[G].err) {
-        st = summ[G].err;
+      }
+      if (!err && !(ev.p_d_y > 0.0)) err = DSDV_E_DRAFTING_CONTRACT;
+      ev.p_eff = p_eff;
+      ev.a = err ? 0.0 : fmin(1.0, p_eff / ev.p_d_y);
+      ev.u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b, (uint32_t)(G + j));
+      accepted = (!err && ev.u < ev.a) ? 1 : 0;
+      if (!err && fabs(ev.u - ev.a) < p.eps_u) near = 1;
+      const size_t pos = (size_t)b * G + j;
+      if (o.key_mask) o.key_mask[pos] = (uint8_t)key;
+      if (o.accepted) o.accepted[pos] = (uint8_t)accepted;
+      if (o.accept_prob) o.accept_prob[pos] = ev.a;
+      if (o.h_target) o.h_target[pos] = ev.h_t;
+      if (o.h_draft) o.h_draft[pos] = ev.h_d;
+      if (o.p_target_y) o.p_target_y[pos] = ev.p_t_y;
+      if (o.p_draft_y) o.p_draft_y[pos] = ev.p_d_y;
+      if (o.norm_match) o.norm_match[pos] = ev.nm;
+      if (o.p_effective_y) o.p_effective_y[pos] = ev.p_eff;
+      if (o.uniform) o.uniform[pos] = ev.u;
+    }
+    double *rr = o.records + ((size_t)b * G1 + j) * kRecordWords;
+    rr[kRecMt] = ev.mt;
+    rr[kRecLst] = ev.lst;
+    rr[kRecMd] = ev.md;
+    rr[kRecLsd] = ev.lsd;
+    rr[kRecLsz] = ev.lsz;
+    rr[kRecFlags] = (double)(kind | (err << 8) | (key << 16));
+    sj = PosSummary{err, key, kind, near, accepted};
+  }
+  // ---- first rejection or error, left to right (verifier.cpp:223-250) ----
+  const bool act = lane < G;
+  const unsigned stop = __ballot_sync(0xffffffffu, act && (sj.err || !sj.accepted));
+  const int k = stop ? __ffs(stop) - 1 : G;
+  const unsigned upto = (k >= 31) ? 0xffffffffu : ((1u << (k + 1)) - 1u);
+  const int keys = __popc(__ballot_sync(0xffffffffu, act && sj.key) & upto);
+  const int nears = __popc(__ballot_sync(0xffffffffu, act && sj.near) & upto);
+  const int err_k = __shfl_sync(0xffffffffu, sj.err, k & 31);
+  const int kind_k = __shfl_sync(0xffffffffu, sj.kind, k & 31);
+  const int err_g = __shfl_sync(0xffffffffu, sj.err, G & 31);
+  if (lane == 0) {
+    int st = DSDV_OK, pos = -1;
+    double u = 0.0;
+    if (k < G) {
+      if (err_k) {
+        st = err_k;
+      } else if (kind_k == DSDV_EFF_DRAFT) {
+        st = DSDV_E_EMPTY_RESIDUAL;  // residual of P_d against itself (verifier.cpp:209-211)
       } else {
-        pos = G;
-        u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b, (uint32_t)(2 * G));
+        pos = k;
+        u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b,
+                                (uint32_t)(G + k + 1));
       }
-      o.accepted_count[b] = k;
-      o.key_count[b] = keys;
-      o.extra_source[b] = (k < G) ? DSDV_EXTRA_RESIDUAL : DSDV_EXTRA_BONUS;
-      o.extra_token[b] = -1;
-      o.status[b] = st;
-      o.near_threshold[b] = nears;
-      position[b] = pos;
-      uniform[b] = u;
-      s_pos = pos;
-      if (pos >= 0) {
-        const double *r = o.records + ((size_t)b * G1 + pos) * kRecordWords;
-        const int kind = (int)r[kRecFlags] & 0xff;
-        PosEval ev;
-        ev.mt = r[kRecMt];
-        ev.lst = r[kRecLst];
-        ev.md = r[kRecMd];
-        ev.lsd = r[kRecLsd];
-        ev.lsz = r[kRecLsz];
-        set_weigher(wf, pos == G ? kWeightPlain
-                                 : (kind == DSDV_EFF_SOFTENED ? kWeightResSoft : kWeightResTarget),
-                    ev, omt, tau);
-      }
+    } else if (err_g) {
+      st = err_g;
+    } else {
+      pos = G;
+      u = dsdv_philox_uniform(p.seed, p.window, p.seq_offset + (uint32_t)b, (uint32_t)(2 * G));
     }
-  }
-  __syncthreads();
-  // ---- this slice's mass of the extra-draw row (fused MASS step) ----
-  const int pos = s_pos;
-  if (pos < 0) {
-    if (threadIdx.x == 0) {
-      put_peers(mass_out + b, 0.0, mpd);
-      if (mpd.n) __threadfence_system();
-    }
-    return;
-  }
-  if (threadIdx.x >= kConsumerThreads) return;
-  const In *rt = target + ((size_t)b * G1 + pos) * (size_t)p.stride;
-  const In *rd = draft + ((size_t)b * G + (pos < G ? pos : 0)) * (size_t)p.stride;
-  int near = 0;
-  cdf_sample<In, Acc>(rt, rd, wf, p.vocab_local, 0.0, p.eps_u, &samp, threadIdx.x, &near, -1.0,
-                      tiles ? tiles + (size_t)b * (kMaxTiles + 2) : nullptr);
-  if (threadIdx.x == 0) {
-    put_peers(mass_out + b, samp.W, mpd);
-    if (mpd.n) __threadfence_system();
+    o.accepted_count[b] = k;
+    o.key_count[b] = keys;
+    o.extra_source[b] = (k < G) ? DSDV_EXTRA_RESIDUAL : DSDV_EXTRA_BONUS;
+    o.extra_token[b] = -1;
+    o.status[b] = st;
+    o.near_threshold[b] = nears;
+    position[b] = pos;
+    uniform[b] = u;
   }
 }
 
@@ -443,7 +395,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
 // rank whose id range holds T = u * W (W summed over slices in shard order)
 // scans its slice; other ranks write -1.
 template <class In>
-__global__ void __launch_bounds__(kConsumerThreads)
+__global__ void __launch_bounds__(kConsumerThreads, 4)
     shard_sample_kernel(const __grid_constant__ DevParams p, int mode, int rank, int nranks,
                         const In *__restrict__ draft, const In *__restrict__ target,
                         const double *__restrict__ records, const int32_t *__restrict__ position,
@@ -464,8 +416,12 @@ __global__ void __launch_bounds__(kConsumerThreads)
     t_local = -1.0;
     if (j < 0 || j > G) {
       skip = 1;
-      if (mode == 0) mass_out[b] = 0.0;
-      else put_peers(token_out + b, -1, tpd);
+      if (mode == 0) {
+        put_peers(mass_out + b, 0.0, tpd);
+        if (tpd.n) __threadfence_system();
+      } else {
+        put_peers(token_out + b, -1, tpd);
+      }
     } else {
       const double *r = records + ((size_t)b * G1 + j) * kRecordWords;
       const int kind = (int)r[kRecFlags] & 0xff;
@@ -520,16 +476,28 @@ __global__ void __launch_bounds__(kConsumerThreads)
   const In *rt = target + ((size_t)b * G1 + j) * (size_t)p.stride;
   const In *rd = draft + ((size_t)b * G + (j < G ? j : 0)) * (size_t)p.stride;
   int near = 0;
-  const int idx = cdf_sample<In, Acc>(
-      rt, rd, wf, p.vocab_local, 0.0, p.eps_u, &samp, tid, &near, mode == 1 ? t_local : -1.0,
-      nullptr, (mode == 1 && tiles) ? tiles + (size_t)b * (kMaxTiles + 2) : nullptr);
+  // MASS keeps the tile sums (tiles_out) for this slice's RESOLVE scan
+  double *tiles_b = tiles ? const_cast<double *>(tiles) + (size_t)b * (kMaxTiles + 2) : nullptr;
+  const int idx = cdf_sample<In, Acc>(rt, rd, wf, p.vocab_local, 0.0, p.eps_u, &samp, tid, &near,
+                                      mode == 1 ? t_local : -1.0, mode == 0 ? tiles_b : nullptr,
+                                      mode == 1 ? tiles_b : nullptr, mode == 0, kSliceTileSubs);
   if (tid == 0) {
-    if (mode == 0)
-      mass_out[b] = samp.W;
-    else
+    if (mode == 0) {
+      put_peers(mass_out + b, samp.W, tpd);
+      if (tpd.n) __threadfence_system();
+    } else {
       put_peers(token_out + b, idx < 0 ? -1 : p.vocab_offset + idx, tpd);
+    }
   }
 }
+
+template <class In>
+cudaError_t launch_shard_sample(const DevParams &p, int mode, int rank, int nranks,
+                                const void *draft, const void *target, const double *records,
+                                const int32_t *position, const double *uniform,
+                                const double *masses, double *mass_out, int32_t *token_out,
+                                int32_t *status, const double *tiles, cudaStream_t stream,
+                                const long long *tok_delta, int n_delta, size_t mstride);
 
 template <class In>
 cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const double *topv,
@@ -538,10 +506,8 @@ cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const doub
                                int32_t *position, double *uniform, double *mass_out,
                                double *tiles, cudaStream_t stream, const long long *mass_delta,
                                int n_delta) {
-  if (P < 1 || P > kMaxShards || p.gamma > 31 || n_delta > 8) return cudaErrorInvalidValue;
-  PeerDelta mpd{};
-  mpd.n = n_delta;
-  for (int q = 0; q < n_delta; ++q) mpd.d[q] = mass_delta[q];
+  if (P < 1 || P > kMaxShards || p.gamma > 31 || p.top_m > kMaxTopM || n_delta > 8)
+    return cudaErrorInvalidValue;
   const int G1 = p.gamma + 1;
   MergeIn in{rec, topv, topi, P, (size_t)p.B * G1 * kRecordWords,
              (size_t)p.B * p.gamma * 2 * p.top_m, (size_t)p.B * p.gamma * 2 * p.top_m};
@@ -550,17 +516,34 @@ cudaError_t launch_shard_merge(const DevParams &p, const double *rec, const doub
     in.rec_stride = in.topv_stride = rank_bytes / 8;
     in.topi_stride = rank_bytes / 4;
   }
-  const int threads = 32 * G1 > kConsumerThreads ? 32 * G1 : kConsumerThreads;
-  if (threads <= 320)
-    shard_merge_kernel<In, 320, 4><<<p.B, threads, 0, stream>>>(p, in, (const In *)draft,
-                                                               (const In *)target, tokens, o,
-                                                               position, uniform, mass_out, tiles,
-                                                               mpd);
+  const int grid = (p.B + kDecideWarps - 1) / kDecideWarps;
+  // stage the lists in shared memory while they fit (C4: 7.7 KB per sequence at P=4)
+  size_t stage = ((size_t)P * p.gamma * 2 * p.top_m * 12 + 15) & ~size_t(15);
+  if (stage * kDecideWarps > kDecideStageMax) stage = 0;
+  const size_t dsm = stage * kDecideWarps;
+  cudaError_t e;
+  // (the attribute is per device: set on every launch, a cheap host call)
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t r =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecideStageMax);
+    if (r != cudaSuccess) return r;
+    kern<<<grid, kDecideWarps * 32, dsm, stream>>>(p, in, tokens, o, position, uniform, stage);
+    return cudaSuccess;
+  };
+  if (P <= 2)
+    e = go(shard_decide_kernel<2>);
+  else if (P <= 4)
+    e = go(shard_decide_kernel<4>);
+  else if (P <= 8)
+    e = go(shard_decide_kernel<8>);
   else
-    shard_merge_kernel<In><<<p.B, threads, 0, stream>>>(p, in, (const In *)draft,
-                                                      (const In *)target, tokens, o, position,
-                                                      uniform, mass_out, tiles, mpd);
-  return cudaGetLastError();
+    e = go(shard_decide_kernel<kMaxShards>);
+  if (e != cudaSuccess) return e;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // this slice's mass of the extra-draw row (MASS), tile sums kept for RESOLVE
+  return launch_shard_sample<In>(p, 0, 0, 1, draft, target, o.records, position, uniform, nullptr,
+                                 mass_out, nullptr, nullptr, tiles, stream, mass_delta, n_delta, 0);
 }
 
 template <class In>

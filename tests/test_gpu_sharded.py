@@ -40,6 +40,21 @@ def test_sharded_f32_tau_sweep(verifier, oracle, tau):
     assert rep.ok(), rep.mismatches[:5]
 
 
+@pytest.mark.parametrize("dtype,G,P,top_m", [(torch.float32, 16, 12, 12),
+                                             (torch.bfloat16, 16, 5, 32),
+                                             (torch.bfloat16, 15, 8, 32),
+                                             (torch.float32, 31, 3, 4)])
+def test_sharded_merge_shapes(verifier, oracle, dtype, G, P, top_m):
+    """The decide step's other shapes: gamma + 1 > 16 (one lane per position),
+    more than 8 slices (list heads in local memory), top_m up to 32 with lists
+    too large to stage in shared memory."""
+    crit = Oracle.crit(2.0, 0.2, 0.5, top_m)
+    V = 6000
+    rep, gpu, uns = _run(verifier, oracle, dtype, 6, G, V, 0.3, crit, P, seed=5)
+    assert rep.ok(), rep.mismatches[:5]
+    assert rep.eps_events <= 2
+
+
 def test_sharded_equals_unsharded_gpu(verifier, oracle):
     crit = Oracle.crit(2.0, 0.2, 0.5, 10)
     B, G, V = 160, 8, 128256  # 1,440 items: well above one per CTA
