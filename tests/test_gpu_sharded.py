@@ -55,6 +55,16 @@ def test_sharded_merge_shapes(verifier, oracle, dtype, G, P, top_m):
     assert rep.eps_events <= 2
 
 
+@pytest.mark.parametrize("dtype,P", [(torch.bfloat16, 1), (torch.float32, 2)])
+def test_sharded_long_slices(verifier, oracle, dtype, P):
+    """Slices longer than the deferred top-m selection takes (more than 128
+    stages of 1 KB): the streaming capture path of the slice kernel."""
+    crit = Oracle.crit(2.0, 0.2, 0.5, 10)
+    rep, gpu, uns = _run(verifier, oracle, dtype, 4, 4, 140000, 0.2, crit, P, seed=9)
+    assert rep.ok(), rep.mismatches[:5]
+    assert rep.eps_events <= 2
+
+
 def test_sharded_equals_unsharded_gpu(verifier, oracle):
     crit = Oracle.crit(2.0, 0.2, 0.5, 10)
     B, G, V = 160, 8, 128256  # 1,440 items: well above one per CTA
