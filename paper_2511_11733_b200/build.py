@@ -30,7 +30,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
               f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
 
-CU_SOURCES = ["verify.cu", "rows.cu", "shard.cu", "slice.cu", "topm.cu", "calib.cu", "abi.cu"]
+CU_SOURCES = ["verify.cu", "rows.cu", "shard.cu", "topm.cu", "calib.cu", "abi.cu"]
 HOST_SOURCES = ["dsd_api.cpp", "calib_api.cpp"]
 
 

@@ -27,9 +27,6 @@ template <class In>
 cudaError_t launch_fused(const DevParams &, const void *, const void *, const int32_t *,
                          const DevOut &, const DevScratch &, cudaStream_t, int *);
 template <class In>
-cudaError_t launch_slice_stats(const DevParams &, const void *, const void *, const int32_t *,
-                               const DevOut &, unsigned int *, unsigned int *, cudaStream_t);
-template <class In>
 cudaError_t launch_sample_extra(const DevParams &, const void *, const void *, const double *,
                                 const int32_t *, const double *, int32_t *, int32_t *,
                                 cudaStream_t);
@@ -285,29 +282,6 @@ dsdv_status run_fused(dsdv_ctx *ctx, const dsdv_params *params, const void *draf
   o.topi = topi;
   o.npeer = npeer;
   for (int q = 0; q < npeer; ++q) o.peer_delta[q] = peer_delta[q];
-#ifndef DSDV_SLICE_FUSED
-  if (partial) {
-    // vocabulary slices: one warp per item (slice.cu); the fused kernel with
-    // DSDV_SLICE_FUSED (development comparison)
-    switch (params->dtype) {
-      case DSDV_DTYPE_BF16:
-        e = dsdv::launch_slice_stats<__nv_bfloat16>(d, draft, target, tokens, o, s.ticket,
-                                                     s.exit_count, (cudaStream_t)stream);
-        break;
-      case DSDV_DTYPE_F32:
-        e = dsdv::launch_slice_stats<float>(d, draft, target, tokens, o, s.ticket, s.exit_count,
-                                             (cudaStream_t)stream);
-        break;
-      default:
-        e = dsdv::launch_slice_stats<double>(d, draft, target, tokens, o, s.ticket,
-                                              s.exit_count, (cudaStream_t)stream);
-        break;
-    }
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "slice stats launch");
-    ctx->launches += 1;
-    return DSDV_OK;
-  }
-#endif
   switch (params->dtype) {
     case DSDV_DTYPE_BF16:
       e = dsdv::launch_fused<__nv_bfloat16>(d, draft, target, tokens, o, s, (cudaStream_t)stream,

@@ -57,8 +57,7 @@ def test_sharded_merge_shapes(verifier, oracle, dtype, G, P, top_m):
 
 @pytest.mark.parametrize("dtype,P", [(torch.bfloat16, 1), (torch.float32, 2)])
 def test_sharded_long_slices(verifier, oracle, dtype, P):
-    """Slices longer than the deferred top-m selection takes (more than 128
-    stages of 1 KB): the streaming capture path of the slice kernel."""
+    """Long slices (P=1: whole rows in partial mode) and fp32 halves."""
     crit = Oracle.crit(2.0, 0.2, 0.5, 10)
     rep, gpu, uns = _run(verifier, oracle, dtype, 4, 4, 140000, 0.2, crit, P, seed=9)
     assert rep.ok(), rep.mismatches[:5]
