@@ -57,6 +57,12 @@ cudaError_t launch_peer_signal(char *const *bases, int nranks, int rank, unsigne
                                unsigned long long epoch, cudaStream_t stream);
 cudaError_t launch_peer_wait(const unsigned long long *flags, int nranks, unsigned long long epoch,
                              unsigned long long timeout_ns, int *status, cudaStream_t stream);
+cudaError_t launch_peer_round(char *const *bases, int nranks, int rank, unsigned long long stride,
+                              unsigned long long epoch, const unsigned long long *flags,
+                              unsigned long long timeout_ns, int *status, int reset,
+                              cudaStream_t stream);
+cudaError_t launch_tokens_fold(const int32_t *tok, size_t stride, int nranks, int B, int32_t *out,
+                               const int32_t *peer_status, int32_t *status, cudaStream_t stream);
 cudaError_t launch_status_fold(const int32_t *peer_status, int32_t *status, int batch,
                                cudaStream_t stream);
 cudaError_t launch_log_rows(double *x, size_t n, cudaStream_t stream);
@@ -951,51 +957,50 @@ dsdv_status dsdv_shard_verify_peers(dsdv_ctx *ctx, const dsdv_params *params,
   double *u = (double *)take((size_t)B * 8);
   double *tiles = (double *)take((size_t)B * DSDV_SHARD_TILE_WORDS * 8);
   int32_t *peer_status = (int32_t *)take(4);
-  e = cudaMemsetAsync(peer_status, 0, 4, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "peer status reset");
   const uint64_t set_bytes = (uint64_t)nranks * rank_stride_bytes;
-  void *sets[DSDV_MAX_PEERS], *flags[DSDV_MAX_PEERS];
-  for (int q = 0; q < nranks; ++q) {
-    sets[q] = (char *)buffer_bases[q] + (window_epoch & 1) * set_bytes;
-    // dsdv_peer_signal / dsdv_peer_wait find the flags at nranks * stride past this
-    flags[q] = (char *)buffer_bases[q] + 2 * set_bytes - set_bytes;
-  }
+  void *sets[DSDV_MAX_PEERS];
+  for (int q = 0; q < nranks; ++q) sets[q] = (char *)buffer_bases[q] + (window_epoch & 1) * set_bytes;
+  // the arrival flags: nranks * stride past the second set of each buffer
+  // (where dsdv_peer_signal / dsdv_peer_wait find them too)
+  char *flag_bases[DSDV_MAX_PEERS];
+  for (int q = 0; q < nranks; ++q) flag_bases[q] = (char *)buffer_bases[q] + set_bytes;
+  const unsigned long long *own_flags =
+      (const unsigned long long *)((char *)buffer_bases[rank] + 2 * set_bytes);
   const uint64_t f = 3 * window_epoch;
+  cudaStream_t cs = (cudaStream_t)stream;
+  // one launch per flag round: signal, then wait (the first round of the
+  // window also clears the timeout status)
+  auto round = [&](uint64_t epoch, int reset) -> dsdv_status {
+    cudaError_t re = dsdv::launch_peer_round(flag_bases, nranks, rank,
+                                             (unsigned long long)rank_stride_bytes, epoch,
+                                             own_flags, timeout_ns, peer_status, reset, cs);
+    if (re != cudaSuccess) return cuda_fail(ctx, re, "peer round launch");
+    ctx->launches += 1;
+    return DSDV_OK;
+  };
   // 1. stats pass: the records land in every rank's set as items complete
   dsdv_status st = dsdv_shard_stats_peers(ctx, params, draft_logits, target_logits, draft_tokens,
                                           nranks, rank, sets, rank_stride_bytes, o_rec, o_tv,
                                           o_ti, stream);
-  if (st == DSDV_OK) st = dsdv_peer_signal(ctx, nranks, rank, flags, rank_stride_bytes, f, stream);
-  if (st == DSDV_OK)
-    st = dsdv_peer_wait(ctx, nranks, flags[rank], rank_stride_bytes, f, timeout_ns, peer_status,
-                        stream);
+  if (st == DSDV_OK) st = round(f, 1);
   // 2. merge (identical on every rank) + this slice's extra-draw masses
   if (st == DSDV_OK)
     st = dsdv_shard_merge_peers(ctx, params, nranks, rank, sets, rank_stride_bytes, o_rec, o_tv,
                                 o_ti, o_mass, draft_logits, target_logits, draft_tokens, out,
                                 position, u, tiles, stream);
-  if (st == DSDV_OK)
-    st = dsdv_peer_signal(ctx, nranks, rank, flags, rank_stride_bytes, f + 1, stream);
-  if (st == DSDV_OK)
-    st = dsdv_peer_wait(ctx, nranks, flags[rank], rank_stride_bytes, f + 1, timeout_ns,
-                        peer_status, stream);
+  if (st == DSDV_OK) st = round(f + 1, 0);
   // 3. the owning slice resolves the extra token; tokens max over the ranks
   if (st == DSDV_OK)
     st = dsdv_shard_resolve_peers(ctx, params, nranks, rank, sets, rank_stride_bytes, o_mass,
                                   o_tok, draft_logits, target_logits, out->records, position, u,
                                   out->status, tiles, stream);
-  if (st == DSDV_OK)
-    st = dsdv_peer_signal(ctx, nranks, rank, flags, rank_stride_bytes, f + 2, stream);
-  if (st == DSDV_OK)
-    st = dsdv_peer_wait(ctx, nranks, flags[rank], rank_stride_bytes, f + 2, timeout_ns,
-                        peer_status, stream);
-  if (st == DSDV_OK)
-    st = dsdv_peer_tokens_max(ctx, nranks, sets[rank], rank_stride_bytes, o_tok, B,
-                              out->extra_token, stream);
+  if (st == DSDV_OK) st = round(f + 2, 0);
   if (st != DSDV_OK) return st;
-  // a timed-out flag round fails every sequence of the window
-  e = dsdv::launch_status_fold(peer_status, out->status, B, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "status fold launch");
+  // 4. tokens max, and a timed-out flag round fails every sequence
+  e = dsdv::launch_tokens_fold((const int32_t *)((const char *)sets[rank] + o_tok),
+                               (size_t)(rank_stride_bytes / 4), nranks, B, out->extra_token,
+                               peer_status, out->status, cs);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "tokens fold launch");
   ctx->launches += 1;
   return DSDV_OK;
 }

@@ -646,6 +646,71 @@ cudaError_t launch_peer_wait(const unsigned long long *flags, int nranks, unsign
   return cudaGetLastError();
 }
 
+// One flag round in one launch (dsdv_shard_verify_peers): flag `rank` of every
+// rank's buffer = epoch (release, system scope), then hold the stream until
+// every rank's flag in this buffer reached epoch (acquire; a timeout sets
+// *status). reset: the window's first round clears *status first.
+__global__ void peer_round_kernel(PeerBases pb, int nranks, int rank, unsigned long long stride,
+                                  unsigned long long epoch, const unsigned long long *flags,
+                                  unsigned long long timeout_ns, int *status, int reset) {
+  const int q = threadIdx.x;
+  if (reset && q == 0) *status = 0;
+  if (q < nranks) {
+    __threadfence_system();
+    unsigned long long *f =
+        reinterpret_cast<unsigned long long *>(pb.base[q] + (size_t)nranks * stride) + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+  }
+  __syncwarp();
+  if (q < nranks) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+      if (v >= epoch) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicExch(status, DSDV_E_NCCL);
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
+}
+
+cudaError_t launch_peer_round(char *const *bases, int nranks, int rank, unsigned long long stride,
+                              unsigned long long epoch, const unsigned long long *flags,
+                              unsigned long long timeout_ns, int *status, int reset,
+                              cudaStream_t stream) {
+  PeerBases pb{};
+  for (int q = 0; q < nranks; ++q) pb.base[q] = bases[q];
+  peer_round_kernel<<<1, 32, 0, stream>>>(pb, nranks, rank, stride, epoch, flags, timeout_ns,
+                                          status, reset);
+  return cudaGetLastError();
+}
+
+// The window's last step (dsdv_shard_verify_peers): token[b] = max over the
+// ranks' RESOLVE outputs, and a timed-out flag round fails every sequence.
+__global__ void tokens_fold_kernel(const int32_t *tok, size_t stride, int nranks, int B,
+                                   int32_t *out, const int32_t *peer_status, int32_t *status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int32_t m = -1;
+  for (int q = 0; q < nranks; ++q) m = max(m, tok[(size_t)q * stride + b]);
+  out[b] = m;
+  if (*peer_status != 0) status[b] = DSDV_E_NCCL;
+}
+
+cudaError_t launch_tokens_fold(const int32_t *tok, size_t stride, int nranks, int B, int32_t *out,
+                               const int32_t *peer_status, int32_t *status, cudaStream_t stream) {
+  tokens_fold_kernel<<<(B + 255) / 256, 256, 0, stream>>>(tok, stride, nranks, B, out,
+                                                          peer_status, status);
+  return cudaGetLastError();
+}
+
 // token[b] = max over ranks of their RESOLVE outputs (-1 where not the owner)
 __global__ void tokens_max_kernel(const int32_t *tok, size_t stride, int nranks, int B,
                                   int32_t *out) {
