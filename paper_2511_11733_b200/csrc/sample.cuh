@@ -325,12 +325,35 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
     const double T = sh->T, W = sh->W;
     double run = sh->base;
     bool done = false;
+    // the first kPre sub-tiles' loads are issued together (one round trip)
+    constexpr int kPre = 4;
+    uint4 pre_t[kPre], pre_d[kPre];
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+      const int base = (ct * G + k) * sub + lane * VEC;
+      const bool ok = k < G && base < n;
+      pre_t[k] = ok ? ldg128(row_t + base) : make_uint4(0, 0, 0, 0);
+      pre_d[k] = (ok && two_rows) ? ldg128(row_d + base) : make_uint4(0, 0, 0, 0);
+    }
     for (int g = 0; g < G && !done; ++g) {
       const int base = (ct * G + g) * sub + lane * VEC;
       Acc w[VEC];
       const bool ok = base < n;
-      const uint4 rt = ok ? ldg128(row_t + base) : make_uint4(0, 0, 0, 0);
-      const uint4 rd = (ok && two_rows) ? ldg128(row_d + base) : make_uint4(0, 0, 0, 0);
+      uint4 rt, rd;
+      if (g < kPre) {
+        // static selection (no dynamic index into the register arrays)
+        rt = pre_t[0];
+        rd = pre_d[0];
+#pragma unroll
+        for (int k = 1; k < kPre; ++k)
+          if (g == k) {
+            rt = pre_t[k];
+            rd = pre_d[k];
+          }
+      } else {
+        rt = ok ? ldg128(row_t + base) : make_uint4(0, 0, 0, 0);
+        rd = (ok && two_rows) ? ldg128(row_d + base) : make_uint4(0, 0, 0, 0);
+      }
       if (ok) {
         vec_weights<In, Acc>(rt, rd, base, n, wf, w);
       } else {
