@@ -172,3 +172,34 @@ def test_pipeline_emulation_across_processes():
         assert d["gpus"] == n
         assert abs(d["measured"]["R_comm"] - d["des"]["R_comm"]) < 0.03, d
         assert d["measured"]["sync_rounds_dsd"] < d["measured"]["sync_rounds_standard"]
+
+
+def test_one_call_window_times_out_into_statuses(verifier):
+    """dsdv_shard_verify_peers with a peer that never signals: every flag round
+    gives up after timeout_ns and the window's statuses all read DSDV_E_NCCL
+    (never a stale window reported as a success)."""
+    import ctypes as C
+
+    from paper_2511_11733_b200 import dsdv
+    from paper_2511_11733_b200.dsdv import VerifyParams, WindowResult
+    from paper_2511_11733_b200.sharded import (PeerExchange, ShardedVerifier,
+                                               contiguous_slice, slice_bounds)
+    B, G, V, P = 8, 4, 5000, 2
+    draft, target = verifier.synth_logits(B, G, V, torch.bfloat16, logits_seed=5)
+    p = VerifyParams(gamma=G, tau=0.2, seed=1)
+    tokens = verifier.draft_sample(draft, p, vocab=V)
+    lo, n = slice_bounds(V, P, 0)
+    d, t = contiguous_slice(draft, lo, n), contiguous_slice(target, lo, n)
+    sv = ShardedVerifier(verifier)
+    _, size = sv.exchange_layout(B, G, p.top_m)
+    ex = PeerExchange(verifier, P, 0, size, bases=PeerExchange.allocate_local(verifier, P, size))
+    out = WindowResult.allocate(B, G, draft.device, True, records=True)
+    cp = sv._cp(p, d, t, tokens, V, lo, n)
+    bases = (C.c_void_p * P)(*ex.bases)
+    cs = torch.cuda.current_stream()
+    st = dsdv.LIB.dsdv_shard_verify_peers(verifier._h, C.byref(cp), d.data_ptr(), t.data_ptr(),
+                                          tokens.data_ptr(), P, 0, bases, ex.stride, 1,
+                                          int(20e6), C.byref(out._c), cs.cuda_stream)
+    assert st == dsdv.OK
+    torch.cuda.synchronize()
+    assert bool((out.status.cpu() == dsdv.E_NCCL).all())
