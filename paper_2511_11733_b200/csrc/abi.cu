@@ -63,8 +63,6 @@ cudaError_t launch_peer_round(char *const *bases, int nranks, int rank, unsigned
                               cudaStream_t stream);
 cudaError_t launch_tokens_fold(const int32_t *tok, size_t stride, int nranks, int B, int32_t *out,
                                const int32_t *peer_status, int32_t *status, cudaStream_t stream);
-cudaError_t launch_status_fold(const int32_t *peer_status, int32_t *status, int batch,
-                               cudaStream_t stream);
 cudaError_t launch_log_rows(double *x, size_t n, cudaStream_t stream);
 cudaError_t launch_hop_send(unsigned long long t1_ns, int32_t *dst_payload, const int32_t *payload,
                             unsigned long long *dst_flag, unsigned long long value,

@@ -727,17 +727,6 @@ cudaError_t launch_tokens_max(const int32_t *tok, size_t stride, int nranks, int
   return cudaGetLastError();
 }
 
-// a timed-out flag round (dsdv_peer_wait status) fails every sequence
-__global__ void status_fold_kernel(const int32_t *peer_status, int32_t *status, int B) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b < B && *peer_status != 0) status[b] = DSDV_E_NCCL;
-}
-
-cudaError_t launch_status_fold(const int32_t *peer_status, int32_t *status, int batch,
-                               cudaStream_t stream) {
-  status_fold_kernel<<<(batch + 255) / 256, 256, 0, stream>>>(peer_status, status, batch);
-  return cudaGetLastError();
-}
 
 // ---- pipeline emulation hops ----
 // One link of the pipeline: the injected latency t1 (a device spin), then the
