@@ -370,12 +370,23 @@ def run_ours(args, rank, world, local_rank):
                      "frac": achieved / hbm, "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback",
-                     "note": "bf16 at tau in (0,1) is compute-bound before HBM: 3 exps per element pair (2.75 on MUFU); the fold alone, data in shared memory, runs at 5.9 TB/s equivalent (DESIGN.md section 3)"},
+                     "note": "bf16 at tau in (0,1) is compute-bound before HBM: 3 exponentials per element pair, all on MUFU; the fold alone, data in shared memory, runs at 5.9 TB/s equivalent (DESIGN.md section 3)"},
         "e2e": {"value": world * B * GAMMA / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
     }
+    # the second bound: exponentials on the MUFU pipe (0.5 warp-instructions per
+    # clock per SM measured, scripts/micro/pipes.cu) at the sampled SM clock
+    exps = (3 * GAMMA + 1) * B * V  # t, d and the softened mix per pair; bonus row t
+    mhz = line["clocks"].get("sm_mhz") or 1965.0
+    sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+    peak_exp = sms * 16 * mhz * 1e6 / 1e9
+    line["roofline"]["exp_pipe"] = {
+        "achieved": exps / (ms * 1e-3) / 1e9, "peak": peak_exp, "unit": "Gexp/s",
+        "frac": exps / (ms * 1e-3) / 1e9 / peak_exp, "exps_per_launch": exps,
+        "note": "algorithmic exponentials of the first pass (sample items add ~10%); "
+                "peak = SMs x 16 MUFU.EX2 lanes per clock"}
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if parity is not None:
