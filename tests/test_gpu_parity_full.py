@@ -63,6 +63,26 @@ def test_c2_full_window_every_sequence(verifier, oracle, seed, window):
     assert same_k >= B - rep.eps_events
 
 
+@pytest.mark.parametrize("tau,crit_args", [(0.0, (2.0, 0.2, 0.5, 10)),
+                                           (0.5, (1.2, 0.05, 0.8, 4)),
+                                           (1.0, (2.0, 0.2, 0.5, 10)),
+                                           (0.2, (float("inf"), 1.0, 0.0, 32))])
+def test_c2_window_tau_and_criteria(verifier, oracle, tau, crit_args):
+    """The C2 window at the tau endpoints (no mix sum), a key-heavy criterion
+    set, and no key criterion at all with the widest warp selection (m = 32)."""
+    B, G, V = 256, 8, 128256
+    crit = Oracle.crit(*crit_args)
+    draft, target, tokens = _window(verifier, torch.bfloat16, B, G, V, 77, 4, 2)
+    gpu = gpu_window(verifier, draft, target, tokens, V, tau, crit, 4, 2)
+    ref = oracle.verify_batch(host_logits(draft), host_logits(target), tokens.cpu().numpy(),
+                              [(tau, crit)], window_uniforms(4, 2, B, G), V,
+                              all_positions=True)[0]
+    rep = compare_batch(ref, gpu)
+    _report(rep, f"C2 tau={tau} crit={crit_args}")
+    assert rep.ok(), rep.mismatches[:10]
+    assert rep.eps_events <= 3, rep.eps_events
+
+
 def test_c3_full_batch_every_sequence(verifier, oracle):
     """C3 at full size: B=1024, gamma=16, V=151936, fp32 (20.5 GB per window)."""
     B, G, V = 1024, 16, 151936
