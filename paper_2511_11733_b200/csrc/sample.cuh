@@ -170,8 +170,9 @@ __device__ __forceinline__ double warp_sum_f64(double x) {
   return x;
 }
 
-// Weights of the VEC elements at `base` for this lane.
-template <class In, class Acc>
+// Weights of the VEC elements at `base` for this lane (MASK: zero the ids at or
+// past n; a vector wholly inside the row skips it).
+template <class In, class Acc, bool MASK = true>
 __device__ __forceinline__ void vec_weights(const uint4 &rt, const uint4 &rd, int base, int n,
                                             const Weigher<Acc> &wf, Acc (&w)[InTraits<In>::kVec]) {
   constexpr int VEC = InTraits<In>::kVec;
@@ -179,9 +180,11 @@ __device__ __forceinline__ void vec_weights(const uint4 &rt, const uint4 &rd, in
   unpack(rt, vt, (In *)nullptr);
   unpack(rd, vd, (In *)nullptr);
   weigh_vec<VEC>(wf, vt, vd, w);
+  if (MASK) {
 #pragma unroll
-  for (int e = 0; e < VEC; ++e)
-    if (base + e >= n) w[e] = Acc(0);
+    for (int e = 0; e < VEC; ++e)
+      if (base + e >= n) w[e] = Acc(0);
+  }
 }
 
 // Called by all kConsumerThreads threads (thread index `tid` in [0, 256)).
@@ -241,14 +244,19 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
         const int base = ((t + k) * G + g) * sub + lane * VEC;
         if ((t + k) < t1 && base < n) {
           Acc w[VEC];
-          vec_weights<In, Acc>(rt[k], rd[k], base, n, wf, w);
-          // lane sum in the accumulation type, one conversion per vector
+          if (base + VEC <= n)
+            vec_weights<In, Acc, false>(rt[k], rd[k], base, n, wf, w);
+          else
+            vec_weights<In, Acc, true>(rt[k], rd[k], base, n, wf, w);
+          // lane sum in the accumulation type, one conversion per vector; the
+          // last vector with mass is kept (its last supported id is resolved
+          // once, below)
           Acc lv = Acc(0);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            if (w[e] > Acc(0)) last = base + e;
-            lv += w[e];
-          }
+          for (int e = 0; e < VEC; ++e) lv += w[e];
+          // (max, not the latest: with several sub-tiles per tile the
+          // processing order is not the id order)
+          if (lv > Acc(0)) last = max(last, base);
           ls[k] += (double)lv;
         }
       }
@@ -277,6 +285,21 @@ __device__ __noinline__ int cdf_sample(const In *row_t, const In *row_d, const W
     for (int w = 0; w < kConsumerWarps; ++w) {
       W += sh->warp_total[w];
       L = max(L, sh->warp_last[w]);
+    }
+    if (!tiles_in && L >= 0) {
+      // L is the base of the last vector with mass: its last supported id
+      // (the rounding-gap fallback of sample_with_uniform)
+      int e_last = 0;
+      if (lane == 0) {
+        const uint4 rt = ldg128(row_t + L);
+        const uint4 rd = two_rows ? ldg128(row_d + L) : make_uint4(0, 0, 0, 0);
+        Acc w[VEC];
+        vec_weights<In, Acc, true>(rt, rd, L, n, wf, w);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          if (w[e] > Acc(0)) e_last = e;
+      }
+      L += __shfl_sync(0xffffffffu, e_last, 0);
     }
     // t_override >= 0: the boundary was placed by the caller (a vocabulary
     // slice of a sharded row, T relative to this slice's first id)
