@@ -777,9 +777,15 @@ __device__ __forceinline__ void sample_chunk(const uint8_t *sdraft, const uint8_
     }
     Acc w[VEC];
     weigh_vec<VEC>(wf, vt, vd, w);
+    // ids past the row exist only in the row's last chunk
+    if ((chunk + 1) * CH > p.vocab_local) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (id0 + e >= p.vocab_local) w[e] = Acc(0);
+    }
     Acc lv = Acc(0);
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) lv = add_rn(lv, (id0 + e < p.vocab_local) ? w[e] : Acc(0));
+    for (int e = 0; e < VEC; ++e) lv = add_rn(lv, w[e]);
     ls += (double)lv;
   }
   const double ts = warp_sum_f64(ls);
