@@ -58,6 +58,31 @@ def test_tau_endpoints_and_mid(verifier, oracle, tau):
     _check(rep)
 
 
+@pytest.mark.parametrize("V,tau", [(32000, 0.2), (5001, 0.5), (151936, 1.0)])
+def test_fp64_logits_full_window(verifier, oracle, V, tau):
+    """fp64 logit rows through the batched dsdv_verify (the drop-in's row type):
+    fp64 accumulation in the fold, the fp64 sample items, ragged 2-id vectors."""
+    from paper_2511_11733_b200.dsdv import VerifyParams
+    from tests.parity_util import host_rows, oracle_draft_tokens
+    B, G = 12, 4
+    crit = _crit(oracle)
+    d32, t32 = verifier.synth_logits(B, G, V, torch.float32, logits_seed=17)
+    stride = -(-V // 2) * 2  # 16-byte rows of fp64
+    draft = torch.full((B, G, stride), float("-inf"), dtype=torch.float64, device=d32.device)
+    target = torch.full((B, G + 1, stride), float("-inf"), dtype=torch.float64, device=d32.device)
+    draft[..., :V] = d32[..., :V].double()
+    target[..., :V] = t32[..., :V].double()
+    d64, t64 = host_rows(draft, V), host_rows(target, V)
+    toks = oracle_draft_tokens(oracle, d64, 6, 1)
+    tokens = torch.from_numpy(toks).to(draft.device)
+    p = VerifyParams(gamma=G, tau=tau, ratio_limit=crit.ratio_limit, gap_limit=crit.gap_limit,
+                     overlap_floor=crit.overlap_floor, top_m=crit.top_m, seed=6, window=1)
+    out = verifier.verify(draft, target, tokens, p, vocab=V)
+    verifier.sync(p, out, batch=B, vocab=V)
+    rep = compare_window(oracle, d64, t64, toks, out.to_host(), tau, crit, seed=6, window=1)
+    _check(rep)
+
+
 @pytest.mark.parametrize("V", [2, 7, 1000, 4099])
 def test_ragged_vocab(verifier, oracle, V):
     """Vocabularies that are not a multiple of the vector / chunk width."""
