@@ -83,6 +83,34 @@ def test_fp64_logits_full_window(verifier, oracle, V, tau):
     _check(rep)
 
 
+def test_sequence_offset_selects_the_philox_streams(verifier, oracle):
+    """A replica's window (sequence_offset = its first global sequence id) draws
+    the uniforms of those global sequences (the replicas mode of bench.py)."""
+    from paper_2511_11733_b200.dsdv import VerifyParams
+    from tests.parity_util import host_rows, oracle_draft_tokens
+    B, G, V, off = 8, 4, 6000, 1000
+    crit = _crit(oracle)
+    draft, target = verifier.synth_logits(B, G, V, torch.float32, logits_seed=23)
+    d64, t64 = host_rows(draft, V), host_rows(target, V)
+    toks = oracle_draft_tokens(oracle, d64, 9, 2, sequence_offset=off)
+    tokens = torch.from_numpy(toks).to(draft.device)
+    p = VerifyParams(gamma=G, tau=0.3, ratio_limit=crit.ratio_limit, gap_limit=crit.gap_limit,
+                     overlap_floor=crit.overlap_floor, top_m=crit.top_m, seed=9, window=2,
+                     sequence_offset=off)
+    out = verifier.verify(draft, target, tokens, p, vocab=V)
+    verifier.sync(p, out, batch=B, vocab=V)
+    gpu = out.to_host()
+    rep = compare_window(oracle, d64, t64, toks, gpu, 0.3, crit, seed=9, window=2,
+                         sequence_offset=off)
+    _check(rep)
+    # the accept uniforms it used are those of the offset sequences
+    from oracle.oracle_lib import window_uniforms
+    U_off = window_uniforms(9, 2, B, G, off)
+    U_0 = window_uniforms(9, 2, B, G, 0)
+    assert not np.array_equal(U_off, U_0)
+    np.testing.assert_array_equal(gpu["uniform"].reshape(B, G), U_off[:, G:2 * G])
+
+
 @pytest.mark.parametrize("V", [2, 7, 1000, 4099])
 def test_ragged_vocab(verifier, oracle, V):
     """Vocabularies that are not a multiple of the vector / chunk width."""
