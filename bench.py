@@ -368,6 +368,7 @@ def run_ours(args, rank, world, local_rank):
                    "mean_accepted_k": mean_k, "committed_tokens_per_s": world * committed / (ms_max * 1e-3)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
+                     "frac_of_nominal_8tbs": achieved / 8000.0,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback",
                      "note": "bf16 at tau in (0,1) is compute-bound before HBM: 3 exponentials per element pair, all on MUFU; the fold alone, data in shared memory, runs at 5.9 TB/s equivalent (DESIGN.md section 3)"},
