@@ -193,6 +193,29 @@ def check_parity(ver, draft, target, tokens, p, timed_k):
             "checker": "oracle/dsd_oracle.c fp64 (Oracle.verify_batch), every sequence"}
 
 
+def check_parity_sharded(ver, out, tokens, window, Bt, world, device):
+    """A vocabulary-sharded window (every rank holds the same decisions) against
+    the fp64 oracle over the whole rows, every sequence: the eps-band count of
+    this P (the merge order of the slice sums differs from one GPU's)."""
+    import torch
+    from oracle.oracle_lib import Oracle, window_uniforms
+    from tests.parity_util import compare_batch, host_logits
+    crit = Oracle.crit(RATIO, GAP, OVERLAP, TOP_M)
+    gpu = out.to_host()
+    draft_f, target_f = ver.synth_logits(Bt, GAMMA, V, torch.bfloat16, logits_seed=LOGITS_SEED,
+                                         device=device)
+    dh, th = host_logits(draft_f), host_logits(target_f)
+    del draft_f, target_f
+    ref = Oracle().verify_batch(dh, th, tokens.cpu().numpy(), [(TAU, crit)],
+                                window_uniforms(1, window, Bt, GAMMA), V, all_positions=True)[0]
+    rep = compare_batch(ref, gpu)
+    return {"window": int(window), "shards": world, "sequences": rep.sequences,
+            "positions_checked": rep.positions_checked, "mismatches": len(rep.mismatches),
+            "eps_events": rep.eps_events, "device_near_threshold": int(gpu["near_threshold"].sum()),
+            "max_h_rel_err": rep.max_h_err, "max_p_rel_err": rep.max_p_rel_err,
+            "checker": "oracle/dsd_oracle.c fp64 (Oracle.verify_batch) over the unsharded rows"}
+
+
 def make_inputs(ver, device):
     import torch
     from paper_2511_11733_b200.dsdv import VerifyParams
@@ -446,6 +469,7 @@ def run_sharded(args, rank, world, local_rank):
     dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     gpu_launches = ver.launches - launches0
+    timed_window = args.steps - 1  # `out` holds this window's results
     ms_t = torch.tensor([ms], device=device)
     dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
@@ -536,6 +560,10 @@ def run_sharded(args, rank, world, local_rank):
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
     }
+    # the last timed window against the fp64 oracle on the whole rows (rank 0,
+    # after the timed regions; the other ranks are done)
+    if not args.no_cpu:
+        line["parity"] = check_parity_sharded(ver, out, tokens, timed_window, Bt, world, device)
     print(json.dumps(line), flush=True)
 
 
