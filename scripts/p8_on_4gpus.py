@@ -120,7 +120,6 @@ bad = int(sum(int((o.status != 0).sum()) for o in outs))
 parity = None
 if rank == 0:
     # the last window against the fp64 oracle over the unsharded rows
-    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
     from oracle.oracle_lib import Oracle, window_uniforms
     from tests.parity_util import compare_batch, host_logits
     crit = Oracle.crit(p.ratio_limit, p.gap_limit, p.overlap_floor, p.top_m)
