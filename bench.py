@@ -252,12 +252,18 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize(device)
     launches0 = ver.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # one more event after every window: the per-window times (SURVEY 8(d) asks
+    # for the median); the total over the K windows gives `value`
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
         for k in range(args.steps):
             step(k)
+            marks[k].record(stream)
         e1.record(stream)
         torch.cuda.synchronize(device)
+    per_window = [e0.elapsed_time(marks[0])] + [marks[k - 1].elapsed_time(marks[k])
+                                                  for k in range(1, args.steps)]
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -399,6 +405,7 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
+        "ms_per_window_median": statistics.median(per_window),
     }
     # the second bound: exponentials on the MUFU pipe (0.5 warp-instructions per
     # clock per SM measured, scripts/micro/pipes.cu) at the sampled SM clock
